@@ -1,0 +1,242 @@
+"""Pins for the oracle's stencil engine, CH RHS and ADI step.
+
+Independent references: polynomial exactness, sin -> -sin (the cuSten 2d_x_np
+example), stencil composition (Fig 3.1), spectral (FFT) symbols
+of the circulant operators, exact mass conservation, constant fixed points,
+the CN hyperdiffusion amplification factor, and the printed Tables 3.1 / 6.1.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def load_golden(name):
+    rows = []
+    with open(os.path.join(GOLDEN, name)) as fh:
+        for line in fh:
+            if line.strip() and not line.startswith("#"):
+                n, e, o = line.split()
+                rows.append((int(n), float(e), float(o)))
+    return rows
+
+
+# ------------------------------------------------------------------ stencil
+def test_stencil_polynomial_exactness():
+    nx, ny = 16, 3
+    dx = 0.1
+    x = dx * np.arange(nx)
+    g = np.tile(x ** 4, (ny, 1))
+    w = np.array([1, -4, 6, -4, 1]) / dx ** 4
+    out = oracle.stencil_apply(g, w, left=2, right=2, top=0, bottom=0, periodic=False)
+    assert np.allclose(out[:, 2:-2], 24.0, rtol=0, atol=1e-8)
+    assert np.all(out[:, :2] == 0) and np.all(out[:, -2:] == 0)  # untouched
+
+
+def test_stencil_sin_8th_order_example():
+    """cuSten example 2d_x_np: 8th-order d2/dx2 of sin(x) on a
+    1024 x 512 grid, lx = 2 pi, answer -sin(x); 4 boundary cells untouched."""
+    nx, ny = 1024, 512
+    dx = 2 * math.pi / nx
+    x = dx * np.arange(nx)
+    g = np.tile(np.sin(x), (ny, 1))
+    w = np.array([-1 / 560, 8 / 315, -1 / 5, 8 / 5, -205 / 72, 8 / 5, -1 / 5, 8 / 315, -1 / 560]) / dx ** 2
+    sentinel = np.full_like(g, 7.0)
+    out = oracle.stencil_apply(g, w, left=4, right=4, top=0, bottom=0, periodic=False, out=sentinel)
+    assert np.max(np.abs(out[:, 4:-4] + g[:, 4:-4])) < 1e-9
+    assert np.all(out[:, :4] == 7.0) and np.all(out[:, -4:] == 7.0)
+
+
+def test_stencil_composition_fig3_1():
+    """X (1,-2,1) then Y (1,-2,1) equals the Fig 3.1 cross stencil (periodic)."""
+    g = synth.rng(5).standard_normal((2, 12, 10))
+    d2 = np.array([1.0, -2.0, 1.0])
+    gx = oracle.stencil_apply(g, d2, left=1, right=1, top=0, bottom=0)
+    gxy = oracle.stencil_apply(gx, d2, left=0, right=0, top=1, bottom=1)
+    cross = np.array([[1, -2, 1], [-2, 4, -2], [1, -2, 1]], dtype=float)
+    direct = oracle.stencil_apply(g, cross, left=1, right=1, top=1, bottom=1)
+    assert np.max(np.abs(gxy - direct)) < 1e-13
+
+
+def test_stencil_asymmetric_window_and_translation():
+    """Asymmetric window: weight k sits at offset (row r-top, col q-left);
+    a one-hot weight is a pure shift; periodic apply commutes with roll."""
+    g = synth.rng(6).standard_normal((9, 11))
+    w = np.zeros((2, 4))  # top=0, bottom=1, left=1, right=2
+    w[1, 3] = 1.0  # row offset +1, col offset +2
+    out = oracle.stencil_apply(g, w, left=1, right=2, top=0, bottom=1)
+    assert np.array_equal(out, np.roll(np.roll(g, -1, axis=0), -2, axis=1))
+    w2 = synth.rng(7).standard_normal((3, 5))
+    o1 = oracle.stencil_apply(np.roll(g, 3, axis=1), w2, left=2, right=2, top=1, bottom=1)
+    o2 = np.roll(oracle.stencil_apply(g, w2, left=2, right=2, top=1, bottom=1), 3, axis=1)
+    assert np.max(np.abs(o1 - o2)) < 1e-14
+
+
+def test_stencil_rejects_aliasing_and_oversize():
+    g = np.zeros((4, 4))
+    with pytest.raises(oracle.OracleError):
+        oracle.stencil_apply(g, np.ones(5), left=2, right=2, top=0, bottom=0)  # 5 >= nx=4
+    with pytest.raises(oracle.OracleError):
+        oracle.lib()  # ensure loaded
+        rc = oracle.lib().orc_stencil_apply(1, 4, 4, 1, 1, 0, 0, oracle._p(np.ones(3)), 1,
+                                             oracle._p(g), oracle._p(g))
+        oracle._check(rc)
+
+
+# ------------------------------------------------------------------ CH RHS / ADI
+def spectral_symbols(n, dx):
+    th = 2 * np.pi * np.arange(n) / n
+    s2 = 4 * np.sin(th / 2) ** 2  # symbol of -(1,-2,1)
+    sx, sy = np.meshgrid(s2, s2, indexing="xy")
+    lap = -(sx + sy) / dx ** 2
+    bih = (sx + sy) ** 2 / dx ** 4  # = dx^4 + 2 dx^2 dy^2 + dy^4 (r9)
+    return lap, bih
+
+
+def spectral_rhs(cn, cm, dt, D, g, L):
+    n = cn.shape[-1]
+    dx = L / n
+    lap, bih = spectral_symbols(n, dx)
+    cbar = 2 * cn - cm
+    nl = cn ** 3 - cn
+    B = np.real(np.fft.ifft2(bih * np.fft.fft2(cbar)))
+    Lp = np.real(np.fft.ifft2(lap * np.fft.fft2(nl)))
+    return -(2 / 3) * (cn - cm) - (2 / 3) * dt * D * g * B + (2 / 3) * D * dt * Lp
+
+
+def spectral_adi(cn, cm, nsteps, dt, D, g, L):
+    n = cn.shape[-1]
+    dx = L / n
+    sig = (2 / 3) * D * g * dt / dx ** 4
+    th = 2 * np.pi * np.arange(n) / n
+    lam = 1 + 16 * sig * np.sin(th / 2) ** 4
+    lx, ly = np.meshgrid(lam, lam, indexing="xy")
+    cn, cm = cn.copy(), cm.copy()
+    for _ in range(nsteps):
+        R = spectral_rhs(cn, cm, dt, D, g, L)
+        v = np.real(np.fft.ifft2(np.fft.fft2(R) / (lx * ly)))
+        cn, cm = 2 * cn - cm + v, cn
+    return cn, cm
+
+
+def test_ch_rhs_vs_spectral():
+    n, L = 32, 8 * math.pi
+    c0 = synth.ch_ic_random(2, n, seed=3)
+    c1 = c0 + 0.01 * synth.ch_ic_random(2, n, seed=9)
+    dt = synth.ch_dt(n, L)
+    R = oracle.ch_rhs(c1, c0, dt=dt, D=1.0, gamma=0.01, L=L)
+    for s in range(2):
+        ref = spectral_rhs(c1[s], c0[s], dt, 1.0, 0.01, L)
+        assert np.max(np.abs(R[s] - ref)) <= 1e-13 * max(1.0, np.max(np.abs(ref)))
+
+
+@pytest.mark.parametrize("L", [2 * math.pi, 8 * math.pi])
+def test_ch_adi_vs_spectral(L):
+    n = 32
+    c0 = synth.ch_ic_random(1, n, seed=4)[0]
+    dt = synth.ch_dt(n, L)
+    cn, cm = oracle.ch_adi_steps(c0, c0, 10, dt=dt, D=1.0, gamma=0.01, L=L)
+    rn, rm = spectral_adi(c0, c0, 10, dt, 1.0, 0.01, L)
+    assert np.max(np.abs(cn - rn)) <= 1e-12
+    assert np.max(np.abs(cm - rm)) <= 1e-12
+
+
+def test_ch_adi_mass_and_fixed_point():
+    n, L = 48, 4 * math.pi
+    c0 = synth.ch_ic_random(1, n, seed=5)[0]
+    dt = synth.ch_dt(n, L)
+    cn, _ = oracle.ch_adi_steps(c0, c0, 20, dt=dt, D=1.0, gamma=0.01, L=L)
+    assert abs(cn.sum() - c0.sum()) <= 1e-12 * n * n  # mass conserved exactly (§8(c))
+    k = np.full((n, n), 0.3)
+    kn, km = oracle.ch_adi_steps(k, k, 5, dt=dt, D=1.0, gamma=0.01, L=L)
+    assert np.max(np.abs(kn - 0.3)) <= 1e-15 and np.max(np.abs(km - 0.3)) <= 1e-15
+
+
+def test_ch_free_energy_decreases():
+    """F = int (C^4/4 - C^2/2 + gamma/2 |grad C|^2) non-increasing."""
+    n, L, g = 32, 4 * math.pi, 0.01
+    dx = L / n
+    c = synth.ch_ic_random(1, n, seed=6)[0]
+    dt = synth.ch_dt(n, L)
+
+    def F(u):
+        gx = (np.roll(u, -1, 1) - u) / dx
+        gy = (np.roll(u, -1, 0) - u) / dx
+        return np.sum(u ** 4 / 4 - u ** 2 / 2 + g / 2 * (gx ** 2 + gy ** 2)) * dx * dx
+
+    cn, cm = c, c
+    last = F(c)
+    for _ in range(6):
+        cn, cm = oracle.ch_adi_steps(cn, cm, 20, dt=dt, D=1.0, gamma=g, L=L)
+        f = F(cn)
+        assert f <= last + 1e-12
+        last = f
+
+
+def run_ch2d(n, T=10.0, L=2 * math.pi):
+    dt = synth.ch_dt(n, L)
+    c0 = synth.ch_ic_tanh(n, L)
+    cn, _ = oracle.ch_adi_steps(c0, c0, synth.ch_nsteps(T, dt), dt=dt, D=1.0, gamma=0.01, L=L)
+    return cn
+
+
+def test_table_3_1_E128():
+    """Table 3.1: E_128 = 0.1510 (printed to 4 decimals)."""
+    rows = {n: e for n, e, _ in load_golden("table3_1.txt")}
+    e128 = oracle.convergence_error_2d(run_ch2d(128), run_ch2d(64), 2 * math.pi)
+    assert abs(e128 - rows[128]) <= 5e-5
+
+
+@pytest.mark.slow
+def test_table_3_1_E256_E512():
+    rows = {n: e for n, e, _ in load_golden("table3_1.txt")}
+    c128, c256 = run_ch2d(128), run_ch2d(256)
+    assert abs(oracle.convergence_error_2d(c256, c128, 2 * math.pi) - rows[256]) <= 5e-5
+    c512 = run_ch2d(512)
+    assert abs(oracle.convergence_error_2d(c512, c256, 2 * math.pi) - rows[512]) <= 5e-5
+
+
+# ------------------------------------------------------------------ 1D CH and CN hyperdiffusion
+def run_ch1d(n, T=20.0, L=2 * math.pi):
+    dt = synth.ch_dt(n, L)
+    return oracle.ch1d_steps(synth.ch_ic_cos1d(n, L), synth.ch_nsteps(T, dt), n=n, m=1, dt=dt, gamma=0.01, L=L)
+
+
+def test_table_6_1():
+    """Table 6.1 to the printed digits for N = 128..1024, and the
+    order column log2(E_N/E_2N) to 4 decimals (3.7932, 2.0376, 2.0089)."""
+    rows = load_golden("table6_1.txt")
+    runs = {n: run_ch1d(n) for n in (64, 128, 256, 512, 1024, 2048)}
+    E = {n: oracle.convergence_error_1d(runs[n], runs[n // 2], 2 * math.pi) for n in (128, 256, 512, 1024, 2048)}
+    for n, e, order in rows:
+        if n not in E:
+            continue
+        digits = 3 if e < 1e-3 else 4  # printed significant figures
+        assert float(f"{E[n]:.{digits - 1}e}") == pytest.approx(e, rel=1e-9) if e < 1e-3 else round(E[n], 4) == e
+        if n * 2 in E:
+            assert abs(math.log2(E[n] / E[2 * n]) - order) <= 5e-5
+
+
+def test_hyperdiffusion_cn_amplification():
+    """CN hyperdiffusion: per step a mode cos(kx) is multiplied
+    by exactly (1 - 16 s_x S^4)/(1 + 16 s_x S^4), S = sin(pi k/N), s_x = dt/(2dx^4);
+    RHS via the stencil, LHS via the cyclic penta solve."""
+    n, dt, kk = 64, 1e-8, 2
+    dx = 1.0 / n
+    sx = dt / (2 * dx ** 4)
+    x = dx * np.arange(n)
+    c = np.cos(2 * np.pi * kk * x)
+    rhs_w = np.array([-sx, 4 * sx, 1 - 6 * sx, 4 * sx, -sx])
+    A = synth.const_penta(n, sx, -4 * sx, 1 + 6 * sx, -4 * sx, sx)
+    for _ in range(50):
+        f = oracle.stencil_apply(c[None, :], rhs_w, left=2, right=2, top=0, bottom=0)[0]
+        c = oracle.penta_batch_solve(*A, f, n=n, m=1, periodic=True)
+    S = math.sin(math.pi * kk / n)
+    g = (1 - 16 * sx * S ** 4) / (1 + 16 * sx * S ** 4)
+    assert np.max(np.abs(c - g ** 50 * np.cos(2 * np.pi * kk * x))) <= 1e-13
