@@ -1,0 +1,196 @@
+/*
+ * pentab.h — C ABI of libpentab.so, the B200-native (sm_100a) hot path of
+ * Gloster's thesis (arxiv/paper_2101_06550): factor-once/solve-many batched
+ * pentadiagonal and tridiagonal solves (cuPentBatch / cuThomasConstantBatch),
+ * the cuSten-style 2D stencil, and the ADI Cahn–Hilliard time step.
+ *
+ * Citations "P:<lines>" are /root/reference/PAPER.md line numbers with the
+ * thesis section / equation they fall in.
+ *
+ * Conventions (all entry points):
+ *  - extern "C", plain pointers and sizes; every call returns an int status
+ *    (PB_OK or a negative PB_E* code).  pb_last_error() gives details.
+ *  - Data buffers are CALLER-OWNED.  Unless stated otherwise a buffer may be a
+ *    device pointer (cudaMalloc / torch CUDA tensor) or a host pointer
+ *    (pageable or pinned); host buffers are staged through a device scratch
+ *    owned by the library, copies enqueued on `stream`.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  All device work is enqueued on it; hot-path calls
+ *    (pent_solve, tri_solve, stencil_apply, ch_adi_step with device buffers)
+ *    never synchronise the host.
+ *  - Handles are LIBRARY-OWNED and freed by the matching *_destroy.  A
+ *    factored handle is read-only, so concurrent solves on different streams
+ *    are safe.
+ *  - Inputs are never modified except the documented in-place outputs.
+ *  - No CPU fallback: without a usable CUDA device every compute call
+ *    returns PB_ECUDA.
+ */
+#ifndef PENTAB_H
+#define PENTAB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PB_API __attribute__((visibility("default")))
+#else
+#define PB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define PB_OK 0
+#define PB_EINVAL (-1)        /* bad size, pointer, layout, dtype or window   */
+#define PB_EZEROPIVOT (-2)    /* |alpha_i| (or Thomas pivot) < 1e-14  */
+#define PB_ESINGULAR (-3)     /* Navon 2x2 / Sherman–Morrison 1+v.z ~ 0       */
+#define PB_ECUDA (-4)         /* CUDA launch / runtime error, or no device     */
+#define PB_ENOMEM (-5)
+#define PB_EUNSUPPORTED (-6)
+
+/* element types of right-hand sides / solutions / grids */
+#define PB_F64 0
+#define PB_F32 1
+
+/* batch layouts (P:1775-1777 interleaved; P:1955-1956 contiguous) */
+#define PB_INTERLEAVED 0 /* entry i of system s at [i*M + s] (system-fastest)   */
+#define PB_CONTIGUOUS 1  /* entry i of system s at [s*N + i] (one row/system)   */
+
+/* stencil boundaries */
+#define PB_NONPERIODIC 0
+#define PB_PERIODIC 1
+
+typedef struct pb_penta_s *pb_penta_t;
+typedef struct pb_tri_s *pb_tri_t;
+
+/* ------------------------------------------------------------------------
+ * pent_factor — factor once (cuPentBatch factor / cuPentConstantBatch).
+ * P:1686-1708 (§4.2.3, the 14-step LR list) and, if periodic, Navon's
+ * reduction P:1498-1620 (§4.2.2, eq:xhat / eq:solve / eq:first_two).
+ *
+ *  batch      number of systems M the handle will solve (>= 0)
+ *  n          unknowns per system N (>= 5; >= 7 if periodic)
+ *  a..e       fp64 diagonals, each lhs_count*n values, interleaved
+ *             [i*lhs_count + s]; row i of A is
+ *             a_i x_{i-2} + b_i x_{i-1} + c_i x_i + d_i x_{i+1} + e_i x_{i+2}.
+ *             Non-periodic: out-of-band a_0,a_1,b_0,d_{n-1},e_{n-2},e_{n-1}
+ *             are ignored.  Periodic: the same entries are the wrap
+ *             coefficients (row 1: a at column N-1, b at column N; row 2: a at
+ *             column N; row N-1: e at column 1; row N: d at column 1, e at
+ *             column 2), i.e. the matrix of P:1446-1453 when constant.
+ *             Host or device pointers; read only.
+ *  lhs_count  1 = one shared LHS for every system (cuPentConstantBatch,
+ *             P:2204-2222); batch = one LHS per system (cuPentBatch).
+ *  periodic   0 / 1
+ *  dtype      PB_F64 or PB_F32: element type of the right-hand sides the
+ *             handle solves (the factorisation is always computed in fp64 and
+ *             rounded to dtype).
+ *  stream     work (factor + precomputes) is enqueued here; pent_factor
+ *             synchronises this stream once to report pivot errors.
+ *  out        receives the handle (NULL on error).
+ * Errors: PB_EINVAL (sizes/pointers/dtype), PB_EZEROPIVOT (system, row in
+ * pb_last_error), PB_ESINGULAR (Navon 2x2 Schur complement), PB_ECUDA,
+ * PB_ENOMEM.
+ */
+PB_API int pent_factor(int64_t batch, int64_t n, const double *a, const double *b, const double *c,
+                const double *d, const double *e, int64_t lhs_count, int periodic, int dtype,
+                void *stream, pb_penta_t *out);
+
+/* pent_solve — solve A x = f for every system, in place (x overwrites rhs).
+ * P:1710-1729 (forward g, back substitution x) and P:1585-1620 (periodic).
+ *  rhs     batch*n elements of the handle's dtype in `layout`
+ *          (PB_INTERLEAVED or PB_CONTIGUOUS); device or host pointer.
+ * No numeric checks, no host sync for device buffers.  Errors: PB_EINVAL,
+ * PB_ECUDA.                                                              */
+PB_API int pent_solve(pb_penta_t h, void *rhs, int layout, void *stream);
+
+/* pent_solve_many — `count` independent right-hand-side batches laid out
+ * back to back (batch k at rhs + k*batch_stride elements), one launch.     */
+PB_API int pent_solve_many(pb_penta_t h, void *rhs, int layout, int64_t count, int64_t batch_stride,
+                    void *stream);
+
+PB_API int pent_destroy(pb_penta_t h);
+
+/* ------------------------------------------------------------------------
+ * tri_factor / tri_solve / tri_destroy — Thomas algorithm with a shared or
+ * per-system LHS (cuThomasConstantBatch), P:2239-2280 (§5.3.1; the printed
+ * back substitution is corrected to x_i = dhat_i - chat_i x_{i+1}), and for
+ * periodic systems Sherman–Morrison, P:2318-2385 (§5.3.3; A'z = u once).
+ *  a,b,c   fp64 sub/main/super diagonals, lhs_count*n, interleaved.
+ *          Periodic corners: a_0 at (1, N), c_{n-1} at (N, 1).  n >= 3.
+ * Errors as pent_*; 1 + v.z ~ 0 -> PB_ESINGULAR.                          */
+PB_API int tri_factor(int64_t batch, int64_t n, const double *a, const double *b, const double *c,
+               int64_t lhs_count, int periodic, int dtype, void *stream, pb_tri_t *out);
+PB_API int tri_solve(pb_tri_t h, void *rhs, int layout, void *stream);
+PB_API int tri_destroy(pb_tri_t h);
+
+/* ------------------------------------------------------------------------
+ * stencil_apply — cuSten Compute2D{X,Y,XY}{p,np} with linear weights,
+ * P:947-983 (§3.3) and P:1091-1101.
+ *  g        grid descriptor: batch of ny x nx grids, row-major [b][j][i]
+ *           (i = x fastest), element type g->dtype.
+ *  in, out  device or host pointers, must not alias ("the same memory
+ *           cannot be used for both").
+ *  w        window: `left`/`right` points in i, `top` rows above (j-top) and
+ *           `bottom` rows below.  X if top = bottom = 0, Y if left = right =
+ *           0, XY (corners included) otherwise.
+ *  weights  HOST array of (top+bottom+1)*(left+right+1) fp64 weights,
+ *           row-major from the top-left, "left to right in i, row by row in
+ *           j"; at most 15 x 15.
+ *  boundary PB_PERIODIC (wrap both axes) or PB_NONPERIODIC (cells whose
+ *           window leaves the grid are left untouched in `out`).
+ * Errors: PB_EINVAL (aliasing, extents >= grid size, > 15x15), PB_ECUDA.   */
+typedef struct {
+    int64_t batch, ny, nx;
+    int dtype;
+} pb_grid;
+typedef struct {
+    int left, right, top, bottom;
+} pb_window;
+PB_API int stencil_apply(const pb_grid *g, const void *in, void *out, const pb_window *w,
+                  const double *weights, int boundary, void *stream);
+
+/* ------------------------------------------------------------------------
+ * ch_adi_step — nsteps of the ADI Cahn–Hilliard scheme, Eq 3.1
+ * (§3.5.1):
+ *   L_x w = -2/3 (C^n - C^{n-1}) - 2/3 dt D gamma grad^4 Cbar + 2/3 D dt grad^2 (C^3 - C)^n
+ *   L_y v = w ;  C^{n+1} = Cbar + v ;  Cbar = 2 C^n - C^{n-1}
+ *   L_x = I + 2/3 D gamma dt d_xxxx  (cyclic penta (s,-4s,1+6s,-4s,s), s = 2/3 D gamma dt/dx^4)
+ * with the readings of DESIGN.md §3 (dx = L/n; 13-point biharmonic with the
+ * Fig 3.1 cross stencil; 5-point Laplacian; D*gamma on the explicit grad^4).
+ *  s->c_cur, s->c_prev : device pointers to sims*n*n elements ([sim][j][i]);
+ *       the caller initialises both to C^0.  On return they point
+ *       to the newest / previous level (buffers rotate by pointer swap).
+ *  s->work : device scratch of ch_workspace_bytes() bytes, caller-owned.
+ *  p : D, gamma, L (square periodic domain of side L).
+ * L_x = L_y is factored once and cached per (n, dt, D, gamma, L, dtype).
+ * Errors: PB_EINVAL (n < 8, bad pointers), PB_ECUDA.                      */
+typedef struct {
+    int64_t sims, n;
+    int dtype;
+    void *c_cur, *c_prev, *work;
+} pb_ch_state;
+typedef struct {
+    double D, gamma, L;
+} pb_ch_params;
+PB_API int ch_workspace_bytes(int64_t sims, int64_t n, int dtype, size_t *bytes);
+PB_API int ch_adi_step(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nsteps, void *stream);
+
+/* ------------------------------------------------------------------------
+ * diagnostics */
+/* Last error of the calling thread: code, system/row of a pivot failure,
+ * message (NUL-terminated, truncated to len).  Returns the code.          */
+PB_API int pb_last_error(int64_t *sys, int64_t *row, char *msg, size_t len);
+/* Number of kernels this library has launched since load (for the bench's
+ * gpu_launches count); resettable.                                        */
+PB_API int64_t pb_launch_count(void);
+PB_API void pb_reset_launch_count(void);
+/* 0 if a CUDA device is usable, else PB_ECUDA. */
+PB_API int pb_device_ok(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PENTAB_H */

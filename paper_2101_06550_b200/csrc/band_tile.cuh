@@ -1,0 +1,197 @@
+// band_tile.cuh — the shared-LHS tile kernel (band_core + global load/store)
+// and its launcher; instantiated per (dtype, K) in banded_inst_*.cu so the
+// nvcc builds run in parallel.
+#pragma once
+#include "band_core.cuh"
+#include "common.cuh"
+
+namespace pb {
+
+// ---------------------------------------------------------------- handle
+struct Plan {
+    int nt = 0, mr = 0, w = 0, C = 0;
+    int64_t nchunks = 0;
+    void *tab = nullptr, *mfc = nullptr, *mbc = nullptr;  // dtype scan tables (band_core.cuh)
+};
+
+struct Band {
+    int K = 2;  // 2 = penta, 1 = tri
+    int64_t batch = 0, n = 0, lhs_count = 1;
+    int periodic = 0, dtype = PB_F64;
+    // shared LHS
+    int64_t rows_alloc = 0;
+    double *coefD = nullptr;  // fp64 master (rows_alloc x 8)
+    void *coef = nullptr;     // dtype copy (== coefD for fp64)
+    double *scal = nullptr;   // SCAL_LEN
+    Plan plan;
+    int64_t srow[4] = {-1, -1, -1, -1};
+    // per-system LHS
+    void *pcoef = nullptr;    // dtype, [(i*8 + j) * batch + s]
+    double *pscal = nullptr;  // [j * batch + s]
+    bool shared() const { return lhs_count == 1; }
+    ~Band()
+    {
+        if (coef && coef != coefD) cudaFree(coef);
+        cudaFree(coefD);
+        cudaFree(scal);
+        cudaFree(plan.tab);
+        cudaFree(plan.mfc);
+        cudaFree(plan.mbc);
+        cudaFree(pcoef);
+        cudaFree(pscal);
+    }
+};
+
+// ---------------------------------------------------------------- shared-LHS tile kernel
+template <typename T>
+struct TileArgs {
+    CoreArgs<T> core;
+    T *x;
+    int64_t M, bstride;
+};
+
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T *p) { return __ldcs(p); }
+template <typename T>
+__device__ __forceinline__ void st_stream(T *p, T v) { __stcs(p, v); }
+
+template <typename T, int K, int W, int NT, int MR, bool PER, int LAYOUT>
+__global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) band_tile_kernel(const TileArgs<T> A)
+{
+    constexpr int PC = NT / W;
+    constexpr int RC = PC * MR;
+    __shared__ CoreSmem<T, W, PC> S;
+    extern __shared__ __align__(16) unsigned char dyn_smem[];
+    const int tid = threadIdx.x, s = tid % W, p = tid / W;
+    const int C = A.core.C;
+    const int c = (C > 1) ? (int)cg::this_cluster().block_rank() : 0;
+    const int64_t group = blockIdx.x / C;
+    const int64_t sys = group * W + s;
+    const int64_t N = A.core.n, M = A.M;
+    const int64_t row0 = (int64_t)c * RC, r0 = row0 + (int64_t)p * MR;
+    T *X = A.x + (int64_t)blockIdx.y * A.bstride;
+    T v[MR];
+    if (LAYOUT == PB_INTERLEAVED) {
+        // lanes = W consecutive systems of one row: W*sizeof(T) contiguous bytes
+        const bool ok = sys < M;
+        const T *src = X + r0 * M + sys;
+#pragma unroll
+        for (int k = 0; k < MR; ++k) v[k] = (ok && r0 + k < N) ? ld_stream(src + k * M) : T(0);
+    } else {
+        // systems contiguous: coalesced loads along the row, transposed into a
+        // padded smem tile [RC][W+1] (conflict-free both ways)
+        T *tile = reinterpret_cast<T *>(dyn_smem);
+        for (int e = tid; e < W * RC; e += NT) {
+            const int ss = e / RC, rr = e % RC;
+            const int64_t sy = group * W + ss, r = row0 + rr;
+            tile[rr * (W + 1) + ss] = (sy < M && r < N) ? ld_stream(X + sy * N + r) : T(0);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < MR; ++k) v[k] = tile[(p * MR + k) * (W + 1) + s];
+    }
+    band_core<T, K, W, NT, MR, PER>(v, A.core, S, c, s, p, r0);
+    if (LAYOUT == PB_INTERLEAVED) {
+        // opaque stride: recompute the store addresses instead of keeping the
+        // MR load addresses live across the solve (register pressure)
+        int64_t Mo = M;
+        asm volatile("" : "+l"(Mo));
+        if (sys < M) {
+            T *dst = X + r0 * Mo + sys;
+#pragma unroll
+            for (int k = 0; k < MR; ++k)
+                if (r0 + k < N) st_stream(dst + k * Mo, v[k]);
+        }
+    } else {
+        T *tile = reinterpret_cast<T *>(dyn_smem);
+#pragma unroll
+        for (int k = 0; k < MR; ++k) tile[(p * MR + k) * (W + 1) + s] = v[k];
+        __syncthreads();
+        for (int e = tid; e < W * RC; e += NT) {
+            const int ss = e / RC, rr = e % RC;
+            const int64_t sy = group * W + ss, r = row0 + rr;
+            if (sy < M && r < N) st_stream(X + sy * N + r, tile[rr * (W + 1) + ss]);
+        }
+    }
+}
+
+
+struct TileCfg {
+    int nt, mr;
+};
+// fp64: W = 16 systems per CTA (128 B per row); fp32: W = 32 (128 B per row)
+static const TileCfg CFG64[] = {{256, 4}, {256, 8}, {256, 16}, {256, 32}, {512, 32}};
+static const TileCfg CFG32[] = {{256, 8}, {256, 16}, {256, 32}, {256, 64}, {512, 64}};
+constexpr int NCFG = 5;
+
+template <typename KernT>
+static int prep_kernel(KernT kern, size_t dyn, int C)
+{
+    // idempotent attribute setup (cheap; cached by the runtime)
+    // static + dynamic > 48 KB needs the opt-in even when dyn itself is small
+    if (dyn > 0) PB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    if (C > 8) PB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    return PB_OK;
+}
+
+template <typename T, int K, int W, int NT, int MR, bool PER, int LAYOUT>
+static int launch_tile_t(const Band *h, T *x, int64_t count, int64_t bstride, cudaStream_t st)
+{
+    auto kern = band_tile_kernel<T, K, W, NT, MR, PER, LAYOUT>;
+    constexpr int RC = (NT / W) * MR;
+    const int C = h->plan.C;
+    const size_t dyn = LAYOUT == PB_CONTIGUOUS ? (size_t)RC * (W + 1) * sizeof(T) : 0;
+    int rc = prep_kernel(kern, dyn, C);
+    if (rc) return rc;
+    TileArgs<T> A;
+    A.core.coef = (const T *)h->coef;
+    A.core.tab = (const T *)h->plan.tab;
+    A.core.mfc = (const T *)h->plan.mfc;
+    A.core.mbc = (const T *)h->plan.mbc;
+    A.core.scal = h->scal;
+    A.core.n = h->n;
+    A.core.C = C;
+    for (int j = 0; j < 4; ++j) A.core.srow[j] = h->srow[j];
+    A.x = x;
+    A.M = h->batch;
+    A.bstride = bstride;
+    const int64_t groups = (h->batch + W - 1) / W;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(groups * C), (unsigned)count, 1);
+    cfg.blockDim = dim3(NT, 1, 1);
+    cfg.dynamicSmemBytes = dyn;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = C > 1 ? 1 : 0;
+    PB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A));
+    PB_LAUNCH_CHECK();
+    return PB_OK;
+}
+
+template <typename T, int K, int W, int NT, int MR>
+static int launch_tile_l(const Band *h, T *x, int layout, int64_t count, int64_t bstride, cudaStream_t st)
+{
+    const bool per = h->periodic != 0;
+    if (layout == PB_INTERLEAVED)
+        return per ? launch_tile_t<T, K, W, NT, MR, true, PB_INTERLEAVED>(h, x, count, bstride, st)
+                   : launch_tile_t<T, K, W, NT, MR, false, PB_INTERLEAVED>(h, x, count, bstride, st);
+    return per ? launch_tile_t<T, K, W, NT, MR, true, PB_CONTIGUOUS>(h, x, count, bstride, st)
+               : launch_tile_t<T, K, W, NT, MR, false, PB_CONTIGUOUS>(h, x, count, bstride, st);
+}
+
+
+
+int const_penta_band(int64_t n, double sigma, int dtype, int cfg, int C, cudaStream_t st, Band **out);
+
+// per-(dtype, K) entry points, defined in banded_inst_*.cu
+int launch_tile_f64_k2(const Band *h, void *x, int layout, int64_t count, int64_t bstride, cudaStream_t st);
+int launch_tile_f64_k1(const Band *h, void *x, int layout, int64_t count, int64_t bstride, cudaStream_t st);
+int launch_tile_f32_k2(const Band *h, void *x, int layout, int64_t count, int64_t bstride, cudaStream_t st);
+int launch_tile_f32_k1(const Band *h, void *x, int layout, int64_t count, int64_t bstride, cudaStream_t st);
+
+}  // namespace pb

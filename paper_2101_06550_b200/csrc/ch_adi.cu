@@ -1,0 +1,327 @@
+// ch_adi.cu — the ADI Cahn–Hilliard time step of Eq 3.1 as two
+// fused HBM passes per step on sm_100a.
+//
+//   pass A (rows j):    R = -2/3 (C^n - C^{n-1}) - 2/3 dt D gamma grad^4 Cbar
+//                           + 2/3 D dt grad^2 (C^3 - C)^n          (stencil, smem-staged)
+//                       w = L_x^{-1} R along i                      (band_core, cyclic)
+//   pass B (columns i): v = L_y^{-1} w along j                      (band_core, cyclic)
+//                       C^{n+1} = Cbar + v = 2C^n - C^{n-1} + v      (epilogue, into C^{n-1})
+// then the host rotates the level pointers (cuSten Swap).
+//
+// HBM traffic per point and step: pass A reads C^n, C^{n-1} and writes w;
+// pass B reads w, C^n, C^{n-1} and writes C^{n+1}: 7 field passes = 56 B (fp64),
+// the algorithmic minimum of this two-pass design.  The thesis's separate
+// cuSten RHS kernels, combine kernel and the full-grid transpose between the
+// sweeps are gone: pass A transposes through shared memory, and
+// pass B's systems (grid columns) are already in the interleaved layout.
+//
+// Readings: dx = L/n (r1); Cbar = 2C^n - C^{n-1} (r6); the
+// explicit grad^4 carries D*gamma (r5); grad^2 is the 5-point stencil (r8);
+// grad^4 = dx^4 + 2 dx^2 dy^2 + dy^4 with the Fig 3.1 cross stencil (r9).
+#include <string.h>
+
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "band_tile.cuh"
+
+namespace pb {
+
+template <typename T>
+struct AdiArgs {
+    CoreArgs<T> core;
+    const T *cn;
+    T *cm;
+    T *w;
+    int64_t n;
+    T k_dif, k_bih, k_lap;  // R = k_dif (C^n - C^{n-1}) + k_bih BIH(Cbar) + k_lap LAP(C^3 - C)
+};
+
+constexpr int ADI_IB = 32;  // stencil column block
+
+__device__ __forceinline__ int64_t wrapi(int64_t x, int64_t n)
+{
+    while (x < 0) x += n;
+    while (x >= n) x -= n;
+    return x;
+}
+
+template <typename T, int W, int NT, int MR>
+__global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) adi_pass_a(const AdiArgs<T> A)
+{
+    constexpr int PC = NT / W, RC = PC * MR, WP = W + 1, IB = ADI_IB;
+    constexpr int SB = IB + 4, SN = IB + 2;  // staged row strides (Cbar halo 2, NL halo 1)
+    __shared__ CoreSmem<T, W, PC> S;
+    extern __shared__ __align__(16) unsigned char dyn_smem[];
+    T *tile = reinterpret_cast<T *>(dyn_smem);  // [RC][W+1]: R, then w
+    T *cb = tile + RC * WP;                      // [W+4][IB+4] Cbar
+    T *nl = cb + (W + 4) * SB;                   // [W+2][IB+2] C^3 - C
+    T *dl = nl + (W + 2) * SN;                   // [W][IB]     C^n - C^{n-1}
+    const int tid = threadIdx.x, s = tid % W, p = tid / W;
+    const int C = A.core.C;
+    const int c = (C > 1) ? (int)cg::this_cluster().block_rank() : 0;
+    const int64_t n = A.n, j0 = (int64_t)(blockIdx.x / C) * W;
+    const int64_t plane = n * n;
+    const T *Cn = A.cn + (int64_t)blockIdx.y * plane;
+    const T *Cm = A.cm + (int64_t)blockIdx.y * plane;
+    T *Wo = A.w + (int64_t)blockIdx.y * plane;
+    const int64_t ib0 = (int64_t)c * RC;  // first solve row (grid column i) of this CTA
+
+    // ---- stencil RHS into the solve tile, column block by column block
+    for (int ib = 0; ib < RC; ib += IB) {
+        const int64_t i0 = ib0 + ib;
+        const bool live = i0 < n;  // CTA-uniform
+        if (live) {
+            for (int e = tid; e < (W + 4) * SB; e += NT) {
+                const int r = e / SB, q = e % SB;
+                const int64_t idx = wrapi(j0 - 2 + r, n) * n + wrapi(i0 - 2 + q, n);
+                const T cnv = __ldg(Cn + idx), cmv = __ldg(Cm + idx);
+                cb[e] = T(2) * cnv - cmv;
+                if (r >= 1 && r < W + 3 && q >= 1 && q < IB + 3) nl[(r - 1) * SN + (q - 1)] = cnv * cnv * cnv - cnv;
+                if (r >= 2 && r < W + 2 && q >= 2 && q < IB + 2) dl[(r - 2) * IB + (q - 2)] = cnv - cmv;
+            }
+        }
+        __syncthreads();
+        for (int e = tid; e < W * IB; e += NT) {
+            const int jj = e / IB, ii = e % IB;
+            T R = T(0);
+            if (live && i0 + ii < n) {
+                const T *u = cb + (jj + 2) * SB + (ii + 2);
+                // 13-point biharmonic: dx^4 + dy^4 (1,-4,6,-4,1) + 2 x Fig 3.1 cross stencil
+                const T bih = T(20) * u[0] - T(8) * ((u[-1] + u[1]) + (u[-SB] + u[SB])) +
+                              T(2) * ((u[-SB - 1] + u[-SB + 1]) + (u[SB - 1] + u[SB + 1])) +
+                              ((u[-2] + u[2]) + (u[-2 * SB] + u[2 * SB]));
+                const T *q_ = nl + (jj + 1) * SN + (ii + 1);
+                const T lap = (q_[-1] + q_[1]) + (q_[-SN] + q_[SN]) - T(4) * q_[0];
+                R = A.k_dif * dl[jj * IB + ii] + A.k_bih * bih + A.k_lap * lap;
+            }
+            tile[(ib + ii) * WP + jj] = R;
+        }
+        __syncthreads();
+    }
+    // ---- x-sweep: systems = grid rows j0 + s, unknowns along i
+    T v[MR];
+#pragma unroll
+    for (int k = 0; k < MR; ++k) v[k] = tile[(p * MR + k) * WP + s];
+    band_core<T, 2, W, NT, MR, true>(v, A.core, S, c, s, p, ib0 + (int64_t)p * MR);
+#pragma unroll
+    for (int k = 0; k < MR; ++k) tile[(p * MR + k) * WP + s] = v[k];
+    __syncthreads();
+    // ---- w back to the natural [j][i] layout, coalesced along i
+    for (int e = tid; e < W * RC; e += NT) {
+        const int jj = e / RC, ii = e % RC;
+        const int64_t j = j0 + jj, i = ib0 + ii;
+        if (j < n && i < n) __stcg(Wo + j * n + i, tile[ii * WP + jj]);
+    }
+}
+
+template <typename T, int W, int NT, int MR>
+__global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) adi_pass_b(const AdiArgs<T> A)
+{
+    constexpr int PC = NT / W, RC = PC * MR;
+    __shared__ CoreSmem<T, W, PC> S;
+    const int tid = threadIdx.x, s = tid % W, p = tid / W;
+    const int C = A.core.C;
+    const int c = (C > 1) ? (int)cg::this_cluster().block_rank() : 0;
+    const int64_t n = A.n, i = (int64_t)(blockIdx.x / C) * W + s;
+    const int64_t plane = n * n;
+    const T *Wi = A.w + (int64_t)blockIdx.y * plane;
+    const T *Cn = A.cn + (int64_t)blockIdx.y * plane;
+    T *Cm = A.cm + (int64_t)blockIdx.y * plane;
+    const int64_t r0 = (int64_t)c * RC + (int64_t)p * MR;
+    const bool ok = i < n;
+    // ---- y-sweep: systems = grid columns i (interleaved: lanes = consecutive i)
+    T v[MR];
+    {
+        const T *src = Wi + r0 * n + i;
+#pragma unroll
+        for (int k = 0; k < MR; ++k) v[k] = (ok && r0 + k < n) ? __ldcs(src + k * n) : T(0);
+    }
+    band_core<T, 2, W, NT, MR, true>(v, A.core, S, c, s, p, r0);
+    // ---- C^{n+1} = Cbar^{n+1} + v, written over C^{n-1} (same thread reads then writes)
+    int64_t no = n;
+    asm volatile("" : "+l"(no));
+    if (ok) {
+#pragma unroll
+        for (int k = 0; k < MR; ++k) {
+            if (r0 + k < n) {
+                const int64_t idx = (r0 + k) * no + i;
+                const T cnv = __ldcs(Cn + idx), cmv = __ldcs(Cm + idx);
+                __stcs(Cm + idx, (T(2) * cnv - cmv) + v[k]);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- host side
+template <typename T, int W, int NT, int MR>
+static int launch_adi(const Band *h, const AdiArgs<T> &A, int64_t sims, cudaStream_t st, bool pass_a)
+{
+    constexpr int PC = NT / W, RC = PC * MR;
+    const int C = h->plan.C;
+    const int64_t groups = (A.n + W - 1) / W;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(groups * C), (unsigned)sims, 1);
+    cfg.blockDim = dim3(NT, 1, 1);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = C > 1 ? 1 : 0;
+    if (pass_a) {
+        auto kern = adi_pass_a<T, W, NT, MR>;
+        const size_t dyn = sizeof(T) * ((size_t)RC * (W + 1) + (W + 4) * (ADI_IB + 4) + (W + 2) * (ADI_IB + 2) +
+                                        W * ADI_IB);
+        int rc = prep_kernel(kern, dyn, C);
+        if (rc) return rc;
+        cfg.dynamicSmemBytes = dyn;
+        PB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A));
+    } else {
+        auto kern = adi_pass_b<T, W, NT, MR>;
+        int rc = prep_kernel(kern, 0, C);
+        if (rc) return rc;
+        PB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A));
+    }
+    PB_LAUNCH_CHECK();
+    return PB_OK;
+}
+
+template <typename T>
+static int launch_adi_cfg(const Band *h, const AdiArgs<T> &A, int64_t sims, cudaStream_t st, bool pass_a)
+{
+    const int k = h->plan.mr;
+    if (sizeof(T) == 8) {
+        switch (k) {
+            case 0: return launch_adi<T, 16, 256, 4>(h, A, sims, st, pass_a);
+            case 1: return launch_adi<T, 16, 256, 8>(h, A, sims, st, pass_a);
+            case 2: return launch_adi<T, 16, 256, 16>(h, A, sims, st, pass_a);
+            case 3: return launch_adi<T, 16, 256, 32>(h, A, sims, st, pass_a);
+            case 4: return launch_adi<T, 16, 512, 32>(h, A, sims, st, pass_a);
+        }
+    } else {
+        switch (k) {
+            case 0: return launch_adi<T, 32, 256, 8>(h, A, sims, st, pass_a);
+            case 1: return launch_adi<T, 32, 256, 16>(h, A, sims, st, pass_a);
+            case 2: return launch_adi<T, 32, 256, 32>(h, A, sims, st, pass_a);
+            case 3: return launch_adi<T, 32, 256, 64>(h, A, sims, st, pass_a);
+            case 4: return launch_adi<T, 32, 512, 64>(h, A, sims, st, pass_a);
+        }
+    }
+    return set_error(PB_EINVAL, "bad ADI cfg");
+}
+
+// Tile configuration for a sweep of length n: the smallest per-CTA row span
+// that covers n (one CTA per system group), else the largest span with a
+// cluster of ceil(n / span) CTAs (<= 16).
+static int adi_choose(int64_t n, int dtype, int *C)
+{
+    const TileCfg *T = dtype == PB_F64 ? CFG64 : CFG32;
+    const int W = dtype == PB_F64 ? 16 : 32;
+    for (int k = 0; k < NCFG; ++k) {
+        int64_t rc = (int64_t)(T[k].nt / W) * T[k].mr;
+        if (rc >= n) {
+            *C = 1;
+            return k;
+        }
+    }
+    int k = NCFG - 1;
+    int64_t rc = (int64_t)(T[k].nt / W) * T[k].mr;
+    int64_t c = (n + rc - 1) / rc;
+    if (c > MAX_CLUSTER) return -1;
+    *C = (int)c;
+    return k;
+}
+
+static std::mutex g_adi_mu;
+static std::map<std::tuple<int, int64_t, int, uint64_t>, Band *> g_adi_cache;
+
+static int adi_band(int64_t n, double sigma, int dtype, cudaStream_t st, Band **out)
+{
+    int dev = 0;
+    PB_CUDA_TRY(cudaGetDevice(&dev));
+    uint64_t bits;
+    memcpy(&bits, &sigma, sizeof(bits));
+    auto key = std::make_tuple(dev, n, dtype, bits);
+    std::lock_guard<std::mutex> lk(g_adi_mu);
+    auto it = g_adi_cache.find(key);
+    if (it != g_adi_cache.end()) {
+        *out = it->second;
+        return PB_OK;
+    }
+    int C = 1;
+    int k = adi_choose(n, dtype, &C);
+    if (k < 0) return set_error(PB_EUNSUPPORTED, "ADI grid n = %lld exceeds the 16-CTA cluster span", (long long)n);
+    Band *h = nullptr;
+    int rc = const_penta_band(n, sigma, dtype, k, C, st, &h);
+    if (rc) return rc;
+    g_adi_cache[key] = h;
+    *out = h;
+    return PB_OK;
+}
+
+template <typename T>
+static int adi_run(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nsteps, cudaStream_t st)
+{
+    const int64_t n = s->n;
+    const double dx = p->L / (double)n;  // r1
+    const double sigma = (2.0 / 3.0) * p->D * p->gamma * dt / (dx * dx * dx * dx);
+    Band *h = nullptr;
+    int rc = adi_band(n, sigma, s->dtype, st, &h);
+    if (rc) return rc;
+    AdiArgs<T> A;
+    A.core.coef = (const T *)h->coef;
+    A.core.tab = (const T *)h->plan.tab;
+    A.core.mfc = (const T *)h->plan.mfc;
+    A.core.mbc = (const T *)h->plan.mbc;
+    A.core.scal = h->scal;
+    A.core.n = n;
+    A.core.C = h->plan.C;
+    for (int j = 0; j < 4; ++j) A.core.srow[j] = h->srow[j];
+    A.n = n;
+    A.k_dif = T(-2.0 / 3.0);
+    A.k_bih = T(-(2.0 / 3.0) * dt * p->D * p->gamma / (dx * dx * dx * dx));
+    A.k_lap = T((2.0 / 3.0) * p->D * dt / (dx * dx));
+    A.w = (T *)s->work;
+    for (int64_t step = 0; step < nsteps; ++step) {
+        A.cn = (const T *)s->c_cur;
+        A.cm = (T *)s->c_prev;
+        if ((rc = launch_adi_cfg<T>(h, A, s->sims, st, true))) return rc;
+        if ((rc = launch_adi_cfg<T>(h, A, s->sims, st, false))) return rc;
+        void *t = s->c_prev;  // C^{n+1} now lives in the old C^{n-1} buffer
+        s->c_prev = s->c_cur;
+        s->c_cur = t;
+    }
+    return PB_OK;
+}
+
+}  // namespace pb
+
+extern "C" int ch_workspace_bytes(int64_t sims, int64_t n, int dtype, size_t *bytes)
+{
+    using namespace pb;
+    if (!bytes || sims < 0 || n < 8 || (dtype != PB_F64 && dtype != PB_F32)) return set_error(PB_EINVAL, "bad args");
+    *bytes = dtype_size(dtype) * (size_t)sims * (size_t)n * (size_t)n;
+    return PB_OK;
+}
+
+extern "C" int ch_adi_step(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nsteps, void *stream)
+{
+    using namespace pb;
+    if (!s || !p) return set_error(PB_EINVAL, "null state/params");
+    if (s->n < 8 || s->sims < 0 || nsteps < 0) return set_error(PB_EINVAL, "need n >= 8, sims >= 0, nsteps >= 0");
+    if (s->dtype != PB_F64 && s->dtype != PB_F32) return set_error(PB_EINVAL, "bad dtype");
+    if (!(dt > 0) || !(p->L > 0)) return set_error(PB_EINVAL, "dt and L must be positive");
+    if (s->sims > 65535) return set_error(PB_EINVAL, "sims > 65535 per call");
+    if (pb_device_ok() != PB_OK) return PB_ECUDA;
+    if (s->sims == 0 || nsteps == 0) return PB_OK;
+    if (!s->c_cur || !s->c_prev || !s->work || s->c_cur == s->c_prev)
+        return set_error(PB_EINVAL, "c_cur, c_prev, work must be distinct device buffers");
+    if (!is_device_ptr(s->c_cur) || !is_device_ptr(s->c_prev) || !is_device_ptr(s->work))
+        return set_error(PB_EINVAL, "ch_adi_step buffers must be device memory");
+    cudaStream_t st = (cudaStream_t)stream;
+    return s->dtype == PB_F64 ? adi_run<double>(s, dt, p, nsteps, st) : adi_run<float>(s, dt, p, nsteps, st);
+}
