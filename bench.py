@@ -1,0 +1,458 @@
+"""bench.py — throughput of the B200 hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--no-adi] [--dtype f64|f32]
+
+Headline (``value``): the factor-once batched cyclic pentadiagonal solve of
+configs[1] at its largest size (N = 8192 unknowns, batch M = 8192 systems,
+fp64, interleaved layout, the thesis CH matrix sigma = 45.09), in M unknowns/s
+over all ranks.  A "step" is one pent_solve of the whole batch (one kernel
+launch, in place).  The 512 MiB right-hand side is larger than the 126 MB L2,
+so every step streams from HBM (no flush needed).  Multi-GPU: every rank
+solves its own batch (independent systems; no data-path collective) ->
+"scaling": "weak".
+
+Secondary (``ch_adi``): configs[3] — 512 independent Cahn–Hilliard ADI
+simulations at 512^2 (L = 4 pi, fp64), sharded over the ranks (strong), in
+simulation time-steps/s; one step = both fused passes of Eq 3.1 for every sim.
+
+The oracle (``oracle/``) is executed only in the cpu_baseline leg and under
+``--impl reference`` (rank 0, N = 1 for the former), per the task contract.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "penta solve Munknowns/s & % HBM peak; CH ADI timesteps/s at 1/2/4/8 B200"
+PENTA_N = 8192          # configs[1], largest size: N = batch = 8192
+ADI_SIMS, ADI_N = 512, 512   # configs[3]
+ADI_L = ADI_N * synth.DX_STATS  # 4 pi: dx = 2 pi / 256
+CH_D, CH_GAMMA = 1.0, 0.01
+
+
+# ------------------------------------------------------------------ host-side helpers (CPU-testable)
+def shard(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous block [lo, hi) of `total` independent units owned by `rank`."""
+    base, rem = divmod(total, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+def max_over_ranks(x: float, device=None) -> float:
+    """Max of a per-rank scalar (timings are reported as the slowest rank)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, device=None) -> float:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def penta_matvec(a, b, c, d, e, x, periodic=True):
+    """A x for one system with constant-or-vector diagonals (residual check of
+    the bench line; a mat-vec, not a solve)."""
+    n = x.shape[0]
+    idx = np.arange(n)
+    y = c * x
+    for off, diag in ((-2, a), (-1, b), (1, d), (2, e)):
+        j = idx + off
+        if periodic:
+            y = y + diag * x[j % n]
+        else:
+            ok = (j >= 0) & (j < n)
+            y = y + np.where(ok, diag * x[np.clip(j, 0, n - 1)], 0.0)
+    return y
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons through NVML while running."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._th = None
+        self.ok = False
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+            self._th = threading.Thread(target=self._run, daemon=True)
+            self._th.start()
+        except Exception as ex:  # no NVML: recorded as unavailable
+            self.err = str(ex)
+        return self
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for k, bit in self.REASONS.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._th:
+            self._th.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel_key: str):
+    """dram bytes per launch of `kernel_key` from the committed ncu --set full
+    summary (profiles/ncu_traffic.json), else None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(kernel_key)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ CPU oracle legs
+def oracle_penta_sample(budget_s: float, m_sample: int = 64):
+    """The oracle as it stands on a bounded sample of the configs[1] workload:
+    m_sample systems of N = 8192 (the same shared cyclic LHS), repeated until
+    budget_s of CPU time.  Returns unknowns/s, description."""
+    import oracle
+    n = PENTA_N
+    s = synth.SIGMA_STATS
+    diags = synth.const_penta(n, s, -4 * s, 1 + 6 * s, -4 * s, s)
+    f = synth.rhs_uniform(n, m_sample, seed=2)
+    oracle.penta_batch_solve(*diags, f, n=n, m=m_sample, periodic=True)  # warm
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        oracle.penta_batch_solve(*diags, f, n=n, m=m_sample, periodic=True)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    return reps * n * m_sample / el, f"{reps} x oracle.penta_batch_solve of {m_sample} systems x N={n} (cyclic, fp64)"
+
+
+def oracle_adi_sample(budget_s: float, sims: int = 2, steps: int = 1):
+    import oracle
+    c0 = synth.ch_ic_random(sims, ADI_N, seed=4)
+    dt = synth.ch_dt(ADI_N, ADI_L)
+    reps, t0 = 0, time.perf_counter()
+    cn, cm = c0, c0
+    while True:
+        cn, cm = oracle.ch_adi_steps(cn, cm, steps, dt=dt, D=CH_D, gamma=CH_GAMMA, L=ADI_L)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    return reps * sims * steps / el, f"{reps} x oracle.ch_adi_steps({sims} sims x {ADI_N}^2, {steps} step)"
+
+
+# ------------------------------------------------------------------ GPU legs
+def _events(torch, st, n):
+    return [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+
+
+def bench_penta(args, rank, world, dev):
+    import torch
+    import torch.distributed as dist
+    import paper_2101_06550_b200 as pb
+
+    n = m = PENTA_N
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    es = 8 if args.dtype == "f64" else 4
+    s = synth.SIGMA_STATS
+    diags = synth.const_penta(n, s, -4 * s, 1 + 6 * s, -4 * s, s)
+    st = torch.cuda.current_stream(dev)
+    h = pb.pent_factor(*[torch.from_numpy(v).to(dev) for v in diags], batch=m, n=n, periodic=True, dtype=args.dtype)
+    f_host = synth.rhs_uniform(n, m, seed=2 + rank)
+    f_dev = torch.from_numpy(f_host).to(dev, tdt)
+    x = f_dev.clone()
+    # residual of one solve on sampled systems (fp64 mat-vec on the host)
+    h.solve(x)
+    torch.cuda.synchronize(dev)
+    X = x.double().cpu().numpy().reshape(n, m)
+    F = f_dev.double().cpu().numpy().reshape(n, m)
+    res = 0.0
+    for sy in (0, 1, 4097, m - 1):
+        r = penta_matvec(*(v[0] for v in diags), X[:, sy]) - F[:, sy]
+        res = max(res, float(np.max(np.abs(r)) / np.max(np.abs(F[:, sy]))))
+    # warm-up (in-place repeated solves: each step solves the previous result)
+    for _ in range(args.warmup):
+        h.solve(x)
+    torch.cuda.synchronize(dev)
+    ev = _events(torch, st, 2 * args.steps)
+    pb.reset_launch_count()
+    if dist.is_initialized():
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index if dev.index is not None else 0) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(st)
+        for k in range(args.steps):
+            ev[2 * k].record(st)
+            h.solve(x)
+            ev[2 * k + 1].record(st)
+        t1.record(st)
+        torch.cuda.synchronize(dev)
+    launches = pb.launch_count()
+    if dist.is_initialized():
+        dist.barrier()
+    ms_local = t0.elapsed_time(t1)
+    kern_ms = statistics.mean(ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(args.steps))
+    ms = max_over_ranks(ms_local, dev)
+    kern_ms_max = max_over_ranks(kern_ms, dev)
+    units = world * n * m * args.steps
+    value = units / (ms * 1e-3) / 1e6
+    peak, peak_src = measured_peak_hbm()
+    alg_bytes = 2 * es * n * m  # read f once, write x once
+    achieved = alg_bytes / (kern_ms_max * 1e-3) / 1e9
+
+    # e2e: same metric through the public C-ABI call with HOST (pinned) buffers:
+    # H2D of the step's RHS, the solve, D2H of the solution, every step.
+    e2e_steps = max(3, min(args.steps, 10))
+    xh = torch.from_numpy(f_host).to(tdt).pin_memory()
+    h.solve(xh.numpy())  # warm the staging pool
+    if dist.is_initialized():
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    a0.record(st)
+    for _ in range(e2e_steps):
+        h.solve(xh.numpy(), stream=st.cuda_stream)
+    a1.record(st)
+    torch.cuda.synchronize(dev)
+    wall = time.perf_counter() - w0
+    e2e_ms = max_over_ranks(max(a0.elapsed_time(a1), wall * 1e3), dev)
+    e2e_val = world * n * m * e2e_steps / (e2e_ms * 1e-3) / 1e6
+    h.close()
+    del x, f_dev, xh
+    torch.cuda.empty_cache()
+    return {
+        "value": value, "ms_per_step": ms / args.steps, "kern_ms": kern_ms_max, "launches": launches,
+        "residual": res, "clocks": clk.summary(),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(f"band_tile_{args.dtype}"),
+                     "algorithmic_bytes_per_launch": alg_bytes, "kernel": "band_tile_kernel (pent_solve)",
+                     "peak_source": peak_src},
+        "e2e": {"value": round(e2e_val, 2), "unit": "Munknowns/s", "steps": e2e_steps,
+                "h2d_bytes_per_step": es * n * m, "d2h_bytes_per_step": es * n * m,
+                "path": "pent_solve(handle, host pinned rhs) -> library stages H2D, solve, D2H"},
+    }
+
+
+def bench_adi(args, rank, world, dev):
+    import torch
+    import torch.distributed as dist
+    import paper_2101_06550_b200 as pb
+
+    lo, hi = shard(ADI_SIMS, world, rank)
+    sims = hi - lo
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    es = 8 if args.dtype == "f64" else 4
+    dt = synth.ch_dt(ADI_N, ADI_L)
+    # IC U(-0.1, 0.1), sim k seeded 4 + k; generated on the device
+    # from per-sim seeds for speed (parity tests use the host generator)
+    g = torch.Generator(device=dev)
+    c0 = torch.empty((sims, ADI_N, ADI_N), dtype=tdt, device=dev)
+    for k in range(sims):
+        g.manual_seed(4 + lo + k)
+        c0[k].uniform_(-0.1, 0.1, generator=g)
+    state = pb.CHState(c0)
+    del c0
+    st = torch.cuda.current_stream(dev)
+    mass0 = float(state.c_cur.double().sum())
+    for _ in range(args.warmup):
+        pb.ch_adi_step(state, dt, D=CH_D, gamma=CH_GAMMA, L=ADI_L, nsteps=1)
+    torch.cuda.synchronize(dev)
+    steps = args.adi_steps
+    pb.reset_launch_count()
+    if dist.is_initialized():
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index if dev.index is not None else 0) as clk:
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(st)
+        for _ in range(steps):
+            pb.ch_adi_step(state, dt, D=CH_D, gamma=CH_GAMMA, L=ADI_L, nsteps=1)
+        t1.record(st)
+        torch.cuda.synchronize(dev)
+    launches = pb.launch_count()
+    ms = max_over_ranks(t0.elapsed_time(t1), dev)
+    mass1 = float(state.c_cur.double().sum())
+    drift = max_over_ranks(abs(mass1 - mass0) / (ADI_N * ADI_N * max(sims, 1)), dev)
+    peak, peak_src = measured_peak_hbm()
+    alg_bytes = 7 * es * ADI_N * ADI_N * sims  # 7 field passes per point and step
+    achieved = sum_over_ranks(alg_bytes, dev) / world / (ms / steps * 1e-3) / 1e9
+    del state
+    torch.cuda.empty_cache()
+    return {
+        "value": round(ADI_SIMS * steps / (ms * 1e-3), 2), "unit": "sim-timesteps/s",
+        "whole_batch_steps_per_s": round(steps / (ms * 1e-3), 2), "ms_per_step": ms / steps, "steps": steps,
+        "config": {"workload": "configs[3]: 512 CH ADI sims at 512^2, L=4pi, dt=0.1dx, D=1, gamma=0.01",
+                   "sims_per_rank": sims, "scaling": "strong"},
+        "launches": launches, "mean_abs_mass_drift_per_point": drift, "clocks": clk.summary(),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(f"adi_step_{args.dtype}"),
+                     "algorithmic_bytes_per_step": alg_bytes, "kernel": "adi_pass_a + adi_pass_b (one step)",
+                     "peak_source": peak_src},
+    }
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2101_06550_b200 as pb
+    pb.lib()
+    r = bench_penta(args, rank, world, dev)
+    adi = bench_adi(args, rank, world, dev) if not args.no_adi else None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, sample = oracle_penta_sample(args.cpu_budget)
+        va, sa = oracle_adi_sample(args.cpu_budget / 2)
+        cpu = {"value": round(v / 1e6, 3), "unit": "Munknowns/s", "cores": 1, "kind": "oracle",
+               "sample": sample, "ch_adi": {"value": round(va, 3), "unit": "sim-timesteps/s", "sample": sa}}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(r["value"], 2), "unit": "Munknowns/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["ms_per_step"], 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+            "data": "synthetic (seeded U(-1,1) RHS; thesis CH matrix sigma=45.09 at dx=2pi/256)",
+            "config": {"workload": "configs[1]: batched cyclic penta solve, N=8192, batch=8192 per GPU, "
+                                   "factor-once/solve-many, interleaved", "N": PENTA_N, "batch_per_gpu": PENTA_N,
+                       "layout": "interleaved", "l2": "inputs (512 MiB fp64) larger than the 126 MB L2; no flush",
+                       "parallelism": f"independent batches x{world}"},
+            "roofline": r["roofline"], "cpu_baseline": cpu, "e2e": r["e2e"], "gpu_launches": r["launches"],
+            "clocks": r["clocks"], "residual": r["residual"], "ch_adi": adi,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """Reference arm: the CPU oracle as it stands (this tier has no reference
+    implementation), on the same workload/metric, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    n = PENTA_N
+    m_sample = 64
+    s = synth.SIGMA_STATS
+    diags = synth.const_penta(n, s, -4 * s, 1 + 6 * s, -4 * s, s)
+    f = synth.rhs_uniform(n, m_sample, seed=2)
+    for _ in range(args.warmup):
+        oracle.penta_batch_solve(*diags, f, n=n, m=m_sample, periodic=True)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.penta_batch_solve(*diags, f, n=n, m=m_sample, periodic=True)
+    el = time.perf_counter() - t0
+    v = n * m_sample * args.steps / el / 1e6
+    sample = f"each step: oracle.penta_batch_solve of {m_sample} of the 8192 systems, N={n} (cyclic, fp64)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "Munknowns/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "configs[1]: batched cyclic penta solve, N=8192, batch=8192 per GPU, "
+                               "factor-once/solve-many, interleaved", "N": PENTA_N, "batch_per_gpu": PENTA_N},
+        "cpu_baseline": {"value": round(v, 3), "unit": "Munknowns/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(v, 3), "unit": "Munknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--adi-steps", type=int, default=None, help="ADI steps timed (default: --steps)")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--dtype", choices=["f64", "f32"], default="f64")
+    ap.add_argument("--no-adi", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.adi_steps is None:
+        args.adi_steps = args.steps
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
