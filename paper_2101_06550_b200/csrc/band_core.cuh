@@ -56,10 +56,13 @@ struct CoreArgs {
     int64_t srow[4];        // rows whose forward value feeds the periodic 2x2 (-1: unused)
 };
 
+// Carry buffers are [system][chunk] with one pad column, so both the
+// sweep-layout writes (system fastest across lanes) and the scan-layout reads
+// (chunk fastest) are bank-conflict free.
 template <typename T, int W, int PC>
 struct CoreSmem {
-    T cf[PC][W][2];
-    T in[PC][W][2];
+    T cf0[W][PC + 1], cf1[W][PC + 1];
+    T in0[W][PC + 1], in1[W][PC + 1];
     T aggF[MAX_CLUSTER][W][2];
     T aggB[MAX_CLUSTER][W][2];
     T spec[4][W];
@@ -74,25 +77,27 @@ __device__ __forceinline__ T *peer(T *p, int rank)
     return cg::this_cluster().map_shared_rank(p, rank);
 }
 
+// Coefficient rows are read from the CTA's shared-memory copy (stage_coef):
+// every lane of a system group reads the same row, so the loads broadcast.
 template <typename T>
 __device__ __forceinline__ void ldcoef_f(const T *cr, T &f0, T &f1, T &f2)
 {
-    f0 = __ldg(cr + 0);
-    f1 = __ldg(cr + 1);
-    f2 = __ldg(cr + 2);
+    f0 = cr[0];
+    f1 = cr[1];
+    f2 = cr[2];
 }
 template <>
 __device__ __forceinline__ void ldcoef_f<double>(const double *cr, double &f0, double &f1, double &f2)
 {
-    double2 a = __ldg(reinterpret_cast<const double2 *>(cr));
+    double2 a = *reinterpret_cast<const double2 *>(cr);
     f0 = a.x;
     f1 = a.y;
-    f2 = __ldg(cr + 2);
+    f2 = cr[2];
 }
 template <>
 __device__ __forceinline__ void ldcoef_f<float>(const float *cr, float &f0, float &f1, float &f2)
 {
-    float4 a = __ldg(reinterpret_cast<const float4 *>(cr));
+    float4 a = *reinterpret_cast<const float4 *>(cr);
     f0 = a.x;
     f1 = a.y;
     f2 = a.z;
@@ -100,28 +105,53 @@ __device__ __forceinline__ void ldcoef_f<float>(const float *cr, float &f0, floa
 template <typename T>
 __device__ __forceinline__ void ldcoef_b(const T *cr, T &b1, T &b2)
 {
-    b1 = __ldg(cr + 4);
-    b2 = __ldg(cr + 5);
+    b1 = cr[4];
+    b2 = cr[5];
 }
 template <>
 __device__ __forceinline__ void ldcoef_b<double>(const double *cr, double &b1, double &b2)
 {
-    double2 a = __ldg(reinterpret_cast<const double2 *>(cr + 4));
+    double2 a = *reinterpret_cast<const double2 *>(cr + 4);
+    b1 = a.x;
+    b2 = a.y;
+}
+template <>
+__device__ __forceinline__ void ldcoef_b<float>(const float *cr, float &b1, float &b2)
+{
+    float2 a = *reinterpret_cast<const float2 *>(cr + 4);
     b1 = a.x;
     b2 = a.y;
 }
 template <typename T>
 __device__ __forceinline__ void ldcoef_z(const T *cr, T &z1, T &z2)
 {
-    z1 = __ldg(cr + 6);
-    z2 = __ldg(cr + 7);
+    z1 = cr[6];
+    z2 = cr[7];
 }
 template <>
 __device__ __forceinline__ void ldcoef_z<double>(const double *cr, double &z1, double &z2)
 {
-    double2 a = __ldg(reinterpret_cast<const double2 *>(cr + 6));
+    double2 a = *reinterpret_cast<const double2 *>(cr + 6);
     z1 = a.x;
     z2 = a.y;
+}
+template <>
+__device__ __forceinline__ void ldcoef_z<float>(const float *cr, float &z1, float &z2)
+{
+    float2 a = *reinterpret_cast<const float2 *>(cr + 6);
+    z1 = a.x;
+    z2 = a.y;
+}
+
+// Copy the CTA's rc coefficient rows (global, contiguous) into shared memory.
+// Callers synchronise before band_core reads them.
+template <typename T, int NT>
+__device__ __forceinline__ void stage_coef(T *dst, const T *src, int rc)
+{
+    const int nvec = rc * COEF_STRIDE * (int)sizeof(T) / 16;
+    const int4 *s4 = reinterpret_cast<const int4 *>(src);
+    int4 *d4 = reinterpret_cast<int4 *>(dst);
+    for (int e = threadIdx.x; e < nvec; e += NT) d4[e] = __ldg(s4 + e);
 }
 
 
@@ -160,15 +190,17 @@ __device__ __forceinline__ void seg_scan(T &b0, T &b1, int q, const T *P)
 // The solve core.  v[k] holds f for rows r0 .. r0+MR-1 of system lane s on
 // entry and x on exit.  All threads of the CTA (and all CTAs of the cluster)
 // must call it.  c = CTA rank in the cluster; r0 = c*PC*MR + p*MR.
+// cs = the CTA's coefficient rows in shared memory (stage_coef), row 0 =
+// global row c*PC*MR.
 template <typename T, int K, int W, int NT, int MR, bool PER>
 __device__ __forceinline__ void band_core(T (&v)[MR], const CoreArgs<T> &A, CoreSmem<T, W, NT / W> &S,
-                                          int c, int s, int p, int64_t r0)
+                                          const T *cs, int c, int s, int p, int64_t r0)
 {
     constexpr int PC = NT / W;
     static_assert(PC <= 32 && (PC & (PC - 1)) == 0, "chunks per CTA must be a power of two <= 32");
     const int tid = threadIdx.x;
     const int C = A.C;
-    const T *coef = A.coef + r0 * COEF_STRIDE;
+    const T *coef = cs + p * MR * COEF_STRIDE;
     // scan-layout coordinates: system ss, chunk-lane qq (one carry per thread)
     const int ss = tid / PC, qq = tid % PC;
     const T *tab_c = A.tab + (int64_t)c * PC * TAB_STRIDE;
@@ -185,18 +217,18 @@ __device__ __forceinline__ void band_core(T (&v)[MR], const CoreArgs<T> &A, Core
             y0 = y1;
             y1 = g;
         }
-        S.cf[p][s][0] = y0;
-        S.cf[p][s][1] = y1;
+        S.cf0[s][p] = y0;
+        S.cf1[s][p] = y1;
     }
     __syncthreads();
     // ---- 2. forward carry scan: warp segments (chunks), then cluster (DSMEM)
     {
-        T b0 = S.cf[qq][ss][0], b1 = S.cf[qq][ss][1];
+        T b0 = S.cf0[ss][qq], b1 = S.cf1[ss][qq];
         seg_scan<T, PC>(b0, b1, qq, tab_c + qq * TAB_STRIDE + TAB_PF);
         T e0 = __shfl_up_sync(0xffffffffu, b0, 1, PC), e1 = __shfl_up_sync(0xffffffffu, b1, 1, PC);
         if (qq == 0) e0 = e1 = T(0);
-        S.in[qq][ss][0] = e0;
-        S.in[qq][ss][1] = e1;
+        S.in0[ss][qq] = e0;
+        S.in1[ss][qq] = e1;
         if (C > 1 && qq == PC - 1)
             for (int rr = 0; rr < C; ++rr) {
                 T *pa = peer(&S.aggF[c][ss][0], rr);
@@ -210,7 +242,7 @@ __device__ __forceinline__ void band_core(T (&v)[MR], const CoreArgs<T> &A, Core
         __syncthreads();
     // ---- 3. forward sweep with the true inflow: v <- g
     {
-        T y0 = S.in[p][s][0], y1 = S.in[p][s][1];
+        T y0 = S.in0[s][p], y1 = S.in1[s][p];
         if (C > 1) {
             T Y0 = T(0), Y1 = T(0);
             for (int cc = 0; cc < c; ++cc) affine(Y0, Y1, S.aggF[cc][s][0], S.aggF[cc][s][1], A.mfc + cc * 4);
@@ -258,19 +290,19 @@ __device__ __forceinline__ void band_core(T (&v)[MR], const CoreArgs<T> &A, Core
             z1 = z0;
             z0 = xx;
         }
-        S.cf[p][s][0] = z0;
-        S.cf[p][s][1] = z1;
+        S.cf0[s][p] = z0;
+        S.cf1[s][p] = z1;
     }
     __syncthreads();
     // ---- 5. backward carry scan (lanes in reverse chunk order)
     {
         const int q = PC - 1 - qq;
-        T b0 = S.cf[q][ss][0], b1 = S.cf[q][ss][1];
+        T b0 = S.cf0[ss][q], b1 = S.cf1[ss][q];
         seg_scan<T, PC>(b0, b1, qq, tab_c + q * TAB_STRIDE + TAB_PB);
         T e0 = __shfl_up_sync(0xffffffffu, b0, 1, PC), e1 = __shfl_up_sync(0xffffffffu, b1, 1, PC);
         if (qq == 0) e0 = e1 = T(0);
-        S.in[q][ss][0] = e0;
-        S.in[q][ss][1] = e1;
+        S.in0[ss][q] = e0;
+        S.in1[ss][q] = e1;
         if (qq == PC - 1) {  // chunk 0: the CTA's aggregate
             if (C > 1) {
                 for (int rr = 0; rr < C; ++rr) {
@@ -321,7 +353,7 @@ __device__ __forceinline__ void band_core(T (&v)[MR], const CoreArgs<T> &A, Core
     }
     // ---- 6. back substitution with the true inflow (+ periodic correction): v <- x
     {
-        T z0 = S.in[p][s][0], z1 = S.in[p][s][1];
+        T z0 = S.in0[s][p], z1 = S.in1[s][p];
         if (C > 1) {
             T Z0 = T(0), Z1 = T(0);
             for (int cc = C - 1; cc > c; --cc) affine(Z0, Z1, S.aggB[cc][s][0], S.aggB[cc][s][1], A.mbc + cc * 4);

@@ -70,6 +70,8 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) band_tile_kernel(cons
     const int64_t N = A.core.n, M = A.M;
     const int64_t row0 = (int64_t)c * RC, r0 = row0 + (int64_t)p * MR;
     T *X = A.x + (int64_t)blockIdx.y * A.bstride;
+    T *cs = reinterpret_cast<T *>(dyn_smem);       // [RC][8] coefficient rows of this CTA
+    stage_coef<T, NT>(cs, A.core.coef + row0 * COEF_STRIDE, RC);
     T v[MR];
     if (LAYOUT == PB_INTERLEAVED) {
         // lanes = W consecutive systems of one row: W*sizeof(T) contiguous bytes
@@ -80,7 +82,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) band_tile_kernel(cons
     } else {
         // systems contiguous: coalesced loads along the row, transposed into a
         // padded smem tile [RC][W+1] (conflict-free both ways)
-        T *tile = reinterpret_cast<T *>(dyn_smem);
+        T *tile = cs + RC * COEF_STRIDE;
         for (int e = tid; e < W * RC; e += NT) {
             const int ss = e / RC, rr = e % RC;
             const int64_t sy = group * W + ss, r = row0 + rr;
@@ -90,7 +92,8 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) band_tile_kernel(cons
 #pragma unroll
         for (int k = 0; k < MR; ++k) v[k] = tile[(p * MR + k) * (W + 1) + s];
     }
-    band_core<T, K, W, NT, MR, PER>(v, A.core, S, c, s, p, r0);
+    __syncthreads();  // coefficient table (and contiguous tile) staged
+    band_core<T, K, W, NT, MR, PER>(v, A.core, S, cs, c, s, p, r0);
     if (LAYOUT == PB_INTERLEAVED) {
         // opaque stride: recompute the store addresses instead of keeping the
         // MR load addresses live across the solve (register pressure)
@@ -103,7 +106,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) band_tile_kernel(cons
                 if (r0 + k < N) st_stream(dst + k * Mo, v[k]);
         }
     } else {
-        T *tile = reinterpret_cast<T *>(dyn_smem);
+        T *tile = cs + RC * COEF_STRIDE;
 #pragma unroll
         for (int k = 0; k < MR; ++k) tile[(p * MR + k) * (W + 1) + s] = v[k];
         __syncthreads();
@@ -140,7 +143,7 @@ static int launch_tile_t(const Band *h, T *x, int64_t count, int64_t bstride, cu
     auto kern = band_tile_kernel<T, K, W, NT, MR, PER, LAYOUT>;
     constexpr int RC = (NT / W) * MR;
     const int C = h->plan.C;
-    const size_t dyn = LAYOUT == PB_CONTIGUOUS ? (size_t)RC * (W + 1) * sizeof(T) : 0;
+    const size_t dyn = sizeof(T) * ((size_t)RC * COEF_STRIDE + (LAYOUT == PB_CONTIGUOUS ? (size_t)RC * (W + 1) : 0));
     int rc = prep_kernel(kern, dyn, C);
     if (rc) return rc;
     TileArgs<T> A;

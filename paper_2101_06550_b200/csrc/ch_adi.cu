@@ -54,7 +54,8 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) adi_pass_a(const AdiA
     constexpr int SB = IB + 4, SN = IB + 2;  // staged row strides (Cbar halo 2, NL halo 1)
     __shared__ CoreSmem<T, W, PC> S;
     extern __shared__ __align__(16) unsigned char dyn_smem[];
-    T *tile = reinterpret_cast<T *>(dyn_smem);  // [RC][W+1]: R, then w
+    T *cs = reinterpret_cast<T *>(dyn_smem);    // [RC][8] coefficient rows of this CTA
+    T *tile = cs + RC * COEF_STRIDE;             // [RC][W+1]: R, then w
     T *cb = tile + RC * WP;                      // [W+4][IB+4] Cbar
     T *nl = cb + (W + 4) * SB;                   // [W+2][IB+2] C^3 - C
     T *dl = nl + (W + 2) * SN;                   // [W][IB]     C^n - C^{n-1}
@@ -67,6 +68,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) adi_pass_a(const AdiA
     const T *Cm = A.cm + (int64_t)blockIdx.y * plane;
     T *Wo = A.w + (int64_t)blockIdx.y * plane;
     const int64_t ib0 = (int64_t)c * RC;  // first solve row (grid column i) of this CTA
+    stage_coef<T, NT>(cs, A.core.coef + ib0 * COEF_STRIDE, RC);
 
     // ---- stencil RHS into the solve tile, column block by column block
     for (int ib = 0; ib < RC; ib += IB) {
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) adi_pass_a(const AdiA
     T v[MR];
 #pragma unroll
     for (int k = 0; k < MR; ++k) v[k] = tile[(p * MR + k) * WP + s];
-    band_core<T, 2, W, NT, MR, true>(v, A.core, S, c, s, p, ib0 + (int64_t)p * MR);
+    band_core<T, 2, W, NT, MR, true>(v, A.core, S, cs, c, s, p, ib0 + (int64_t)p * MR);
 #pragma unroll
     for (int k = 0; k < MR; ++k) tile[(p * MR + k) * WP + s] = v[k];
     __syncthreads();
@@ -121,9 +123,12 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) adi_pass_b(const AdiA
 {
     constexpr int PC = NT / W, RC = PC * MR;
     __shared__ CoreSmem<T, W, PC> S;
+    extern __shared__ __align__(16) unsigned char dyn_smem[];
+    T *cs = reinterpret_cast<T *>(dyn_smem);  // [RC][8] coefficient rows of this CTA
     const int tid = threadIdx.x, s = tid % W, p = tid / W;
     const int C = A.core.C;
     const int c = (C > 1) ? (int)cg::this_cluster().block_rank() : 0;
+    stage_coef<T, NT>(cs, A.core.coef + (int64_t)c * RC * COEF_STRIDE, RC);
     const int64_t n = A.n, i = (int64_t)(blockIdx.x / C) * W + s;
     const int64_t plane = n * n;
     const T *Wi = A.w + (int64_t)blockIdx.y * plane;
@@ -138,7 +143,8 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) adi_pass_b(const AdiA
 #pragma unroll
         for (int k = 0; k < MR; ++k) v[k] = (ok && r0 + k < n) ? __ldcs(src + k * n) : T(0);
     }
-    band_core<T, 2, W, NT, MR, true>(v, A.core, S, c, s, p, r0);
+    __syncthreads();  // coefficient table staged
+    band_core<T, 2, W, NT, MR, true>(v, A.core, S, cs, c, s, p, r0);
     // ---- C^{n+1} = Cbar^{n+1} + v, written over C^{n-1} (same thread reads then writes)
     int64_t no = n;
     asm volatile("" : "+l"(no));
@@ -174,16 +180,18 @@ static int launch_adi(const Band *h, const AdiArgs<T> &A, int64_t sims, cudaStre
     cfg.numAttrs = C > 1 ? 1 : 0;
     if (pass_a) {
         auto kern = adi_pass_a<T, W, NT, MR>;
-        const size_t dyn = sizeof(T) * ((size_t)RC * (W + 1) + (W + 4) * (ADI_IB + 4) + (W + 2) * (ADI_IB + 2) +
-                                        W * ADI_IB);
+        const size_t dyn = sizeof(T) * ((size_t)RC * COEF_STRIDE + (size_t)RC * (W + 1) + (W + 4) * (ADI_IB + 4) +
+                                        (W + 2) * (ADI_IB + 2) + W * ADI_IB);
         int rc = prep_kernel(kern, dyn, C);
         if (rc) return rc;
         cfg.dynamicSmemBytes = dyn;
         PB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A));
     } else {
         auto kern = adi_pass_b<T, W, NT, MR>;
-        int rc = prep_kernel(kern, 0, C);
+        const size_t dyn = sizeof(T) * (size_t)RC * COEF_STRIDE;
+        int rc = prep_kernel(kern, dyn, C);
         if (rc) return rc;
+        cfg.dynamicSmemBytes = dyn;
         PB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A));
     }
     PB_LAUNCH_CHECK();
