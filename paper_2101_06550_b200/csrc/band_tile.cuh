@@ -14,6 +14,14 @@ struct Plan {
     void *tab = nullptr, *mfc = nullptr, *mbc = nullptr;  // dtype scan tables (band_core.cuh)
 };
 
+// streaming two-phase solve plan (stream_solve.cuh): tables in dtype
+struct StreamPlan {
+    int ok = 0;
+    int nrb = 0, R = 0;
+    void *tab = nullptr, *mft = nullptr, *mbt = nullptr, *hft = nullptr, *gsp = nullptr, *rsp = nullptr;
+    int srb[4] = {-1, -1, -1, -1};
+};
+
 struct Band {
     int K = 2;  // 2 = penta, 1 = tri
     int64_t batch = 0, n = 0, lhs_count = 1;
@@ -24,6 +32,7 @@ struct Band {
     void *coef = nullptr;     // dtype copy (== coefD for fp64)
     double *scal = nullptr;   // SCAL_LEN
     Plan plan;
+    StreamPlan splan;
     int64_t srow[4] = {-1, -1, -1, -1};
     // per-system LHS
     void *pcoef = nullptr;    // dtype, [(i*8 + j) * batch + s]
@@ -39,6 +48,12 @@ struct Band {
         cudaFree(plan.mbc);
         cudaFree(pcoef);
         cudaFree(pscal);
+        cudaFree(splan.tab);
+        cudaFree(splan.mft);
+        cudaFree(splan.mbt);
+        cudaFree(splan.hft);
+        cudaFree(splan.gsp);
+        cudaFree(splan.rsp);
     }
 };
 
@@ -190,6 +205,15 @@ static int launch_tile_l(const Band *h, T *x, int layout, int64_t count, int64_t
 
 
 int const_penta_band(int64_t n, double sigma, int dtype, int cfg, int C, cudaStream_t st, Band **out);
+
+// streaming solve (stream_solve_f64.cu / _f32.cu): geometry per dtype and launchers
+constexpr int STREAM_R = 224;          // tile rows (PC * MR = 32 * 7) for both dtypes
+constexpr int STREAM_MAX_NRB = 64;     // tiles per system the group scan supports
+int stream_build_tables(Band *h, cudaStream_t st);
+int launch_stream_f64(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st);
+int launch_stream_f32(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st);
+int stream_max_ctas_f64(int K, int periodic);
+int stream_max_ctas_f32(int K, int periodic);
 
 // per-(dtype, K) entry points, defined in banded_inst_*.cu
 int launch_tile_f64_k2(const Band *h, void *x, int layout, int64_t count, int64_t bstride, cudaStream_t st);

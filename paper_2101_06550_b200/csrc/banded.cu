@@ -9,6 +9,8 @@
 
 #include <mutex>
 
+#include <cudaTypedefs.h>
+
 #include "band_tile.cuh"
 
 namespace pb {
@@ -318,6 +320,127 @@ __global__ void block_transfer_kernel(const double *mf, const double *mb, int C,
     }
 }
 
+// ---------------------------------------------------------------- streaming-solve tables
+// Tile-level matrices of the streaming solve (stream_solve.cuh), from the fp64
+// coefficients: for a tile of R rows, Mf_t maps the forward inflow
+// (g_{r0-2}, g_{r0-1}) to the outflow, Mb_t maps the backward inflow
+// (x_{r1}, x_{r1+1}) to (x_{r0}, x_{r0+1}), and Hf_t is the response of
+// (x_{r0}, x_{r0+1}) to the forward inflow (zero f, zero backward inflow).
+// gsp[j] is the response of g on spec row j to its tile's forward inflow.
+template <typename T>
+__global__ void tile_tables_kernel(const double *coef, int nrb, int R, int64_t s0, int64_t s1, int64_t s2, int64_t s3,
+                                   T *mft, T *mbt, T *hft, T *gsp, T *rsp)
+{
+    const int tile = blockIdx.x * blockDim.x + threadIdx.x;
+    if (tile >= nrb) return;
+    const int64_t r0 = (int64_t)tile * R;
+    const int64_t srow[4] = {s0, s1, s2, s3};
+    const double *cr = coef + r0 * COEF_STRIDE;
+    T *rf = rsp + (int64_t)tile * 4 * R;   // [RF0, RF1, RB0, RB1][R]
+    for (int col = 0; col < 2; ++col) {
+        // forward from the unit inflow, f = 0; then back substitution, zero backward inflow
+        double g[STREAM_R];
+        double y0 = col == 0, y1 = col == 1;
+        for (int k = 0; k < R; ++k) {
+            const double gg = -cr[k * 8 + 1] * y1 - cr[k * 8 + 2] * y0;
+            y0 = y1;
+            y1 = gg;
+            g[k] = gg;
+            for (int j = 0; j < 4; ++j)
+                if (srow[j] == r0 + k) gsp[j * 2 + col] = (T)gg;
+        }
+        mft[tile * 4 + 0 + col] = (T)y0;
+        mft[tile * 4 + 2 + col] = (T)y1;
+        double z0 = 0, z1 = 0;
+        for (int k = R - 1; k >= 0; --k) {
+            const double x = g[k] - cr[k * 8 + 4] * z0 - cr[k * 8 + 5] * z1;
+            z1 = z0;
+            z0 = x;
+            rf[col * R + k] = (T)x;
+        }
+        hft[tile * 4 + 0 + col] = (T)z0;
+        hft[tile * 4 + 2 + col] = (T)z1;
+        // back substitution of zero from the unit backward inflow
+        z0 = col == 0;
+        z1 = col == 1;
+        for (int k = R - 1; k >= 0; --k) {
+            const double x = -cr[k * 8 + 4] * z0 - cr[k * 8 + 5] * z1;
+            z1 = z0;
+            z0 = x;
+            rf[(2 + col) * R + k] = (T)x;
+        }
+        mbt[tile * 4 + 0 + col] = (T)z0;
+        mbt[tile * 4 + 2 + col] = (T)z1;
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+        cudaGetLastError();
+    });
+    return fn;
+}
+
+// Build the streaming plan of a shared-LHS handle (coefD factored, srow set).
+// Leaves splan.ok = 0 (other kernels serve the solve) when the tiles of one
+// system would not fit in the resident persistent grid.
+int stream_build_tables(Band *h, cudaStream_t st)
+{
+    const bool f64 = h->dtype == PB_F64;
+    const int PC = 32, MR = STREAM_R / PC;
+    const int R = STREAM_R;
+    const int64_t nrb = (h->n + R - 1) / R;
+    const int maxc = f64 ? stream_max_ctas_f64(h->K, h->periodic) : stream_max_ctas_f32(h->K, h->periodic);
+    h->splan.ok = 0;
+    if (maxc <= 0 || nrb > maxc || nrb > STREAM_MAX_NRB || h->rows_alloc < nrb * R || !tensor_map_encoder()) return PB_OK;
+    const size_t es = dtype_size(h->dtype);
+    const int64_t nch = nrb * PC;
+    double *mfD = nullptr, *mbD = nullptr;
+    PB_CUDA_TRY(cudaMallocAsync(&mfD, sizeof(double) * 4 * nch, st));
+    PB_CUDA_TRY(cudaMallocAsync(&mbD, sizeof(double) * 4 * nch, st));
+    PB_CUDA_TRY(cudaMalloc(&h->splan.tab, es * TAB_STRIDE * nch));
+    PB_CUDA_TRY(cudaMalloc(&h->splan.mft, es * 4 * nrb));
+    PB_CUDA_TRY(cudaMalloc(&h->splan.mbt, es * 4 * nrb));
+    PB_CUDA_TRY(cudaMalloc(&h->splan.hft, es * 4 * nrb));
+    PB_CUDA_TRY(cudaMalloc(&h->splan.gsp, es * 8));
+    PB_CUDA_TRY(cudaMalloc(&h->splan.rsp, es * 4 * STREAM_R * nrb));
+    PB_CUDA_TRY(cudaMemsetAsync(h->splan.gsp, 0, es * 8, st));
+    const unsigned g = (unsigned)((nch + 127) / 128), gt = (unsigned)((nrb + 63) / 64);
+    transfer_kernel<<<g, 128, 0, st>>>(h->coefD, nch, MR, mfD, mbD);
+    PB_LAUNCH_CHECK();
+    if (f64) {
+        scan_table_kernel<double><<<g, 128, 0, st>>>(mfD, mbD, nch, PC, (double *)h->splan.tab);
+        PB_LAUNCH_CHECK();
+        tile_tables_kernel<double><<<gt, 64, 0, st>>>(h->coefD, (int)nrb, R, h->srow[0], h->srow[1], h->srow[2],
+                                                      h->srow[3], (double *)h->splan.mft, (double *)h->splan.mbt,
+                                                      (double *)h->splan.hft, (double *)h->splan.gsp,
+                                                      (double *)h->splan.rsp);
+    } else {
+        scan_table_kernel<float><<<g, 128, 0, st>>>(mfD, mbD, nch, PC, (float *)h->splan.tab);
+        PB_LAUNCH_CHECK();
+        tile_tables_kernel<float><<<gt, 64, 0, st>>>(h->coefD, (int)nrb, R, h->srow[0], h->srow[1], h->srow[2],
+                                                     h->srow[3], (float *)h->splan.mft, (float *)h->splan.mbt,
+                                                     (float *)h->splan.hft, (float *)h->splan.gsp,
+                                                     (float *)h->splan.rsp);
+    }
+    PB_LAUNCH_CHECK();
+    PB_CUDA_TRY(cudaFreeAsync(mfD, st));
+    PB_CUDA_TRY(cudaFreeAsync(mbD, st));
+    for (int j = 0; j < 4; ++j) h->splan.srb[j] = h->srow[j] >= 0 ? (int)(h->srow[j] / R) : -1;
+    h->splan.nrb = (int)nrb;
+    h->splan.R = R;
+    h->splan.ok = 1;
+    return PB_OK;
+}
+
 // ---------------------------------------------------------------- one thread per system
 // The thesis's cuPentBatch kernel shape: g stored in place.
 // Used for per-system LHS and for shared LHS beyond the cluster capacity.
@@ -485,6 +608,18 @@ static int factor_impl(Band *h, const double *a, const double *b, const double *
         }
         h->rows_alloc = k >= 0 ? (int64_t)C * rc_rows : n;
         if (h->rows_alloc < n) h->rows_alloc = n;
+        const int64_t stream_rows = (n + STREAM_R - 1) / STREAM_R * STREAM_R;
+        if (h->rows_alloc < stream_rows) h->rows_alloc = stream_rows;
+        if (h->periodic) {
+            if (h->K == 2) {
+                h->srow[0] = n - 4;
+                h->srow[1] = n - 3;
+                h->srow[2] = n - 2;
+                h->srow[3] = n - 1;
+            } else {
+                h->srow[0] = n - 1;
+            }
+        }
         PB_CUDA_TRY(cudaMalloc(&h->coefD, sizeof(double) * COEF_STRIDE * h->rows_alloc));
         PB_CUDA_TRY(cudaMalloc(&h->scal, sizeof(double) * SCAL_LEN));
         factor_shared_kernel<<<1, 1, 0, st>>>(h->K, n, h->periodic, h->rows_alloc, (const double *)sa.dev,
@@ -527,16 +662,7 @@ static int factor_impl(Band *h, const double *a, const double *b, const double *
             PB_CUDA_TRY(cudaFreeAsync(mfD, st));
             PB_CUDA_TRY(cudaFreeAsync(mbD, st));
         }
-        if (h->periodic) {
-            if (h->K == 2) {
-                h->srow[0] = n - 4;
-                h->srow[1] = n - 3;
-                h->srow[2] = n - 2;
-                h->srow[3] = n - 1;
-            } else {
-                h->srow[0] = n - 1;
-            }
-        }
+        if ((rc = stream_build_tables(h, st))) return rc;
     } else {
         const int64_t M = h->batch;
         double *pcD = nullptr;
@@ -593,7 +719,11 @@ static int solve_impl(const Band *h, void *rhs, int layout, int64_t count, int64
     int rc = sx.in(rhs, bytes, st, true);
     if (rc) return rc;
     sx.out_to(rhs);
-    if (h->shared() && h->plan.C > 0)
+    const bool al = (uintptr_t)sx.dev % 16 == 0 && (h->batch * es) % 16 == 0 && (count == 1 || (bstride * es) % 16 == 0);
+    if (h->shared() && layout == PB_INTERLEAVED && h->splan.ok && al && getenv("PB_STREAM") && !getenv("PB_NO_STREAM"))
+        rc = h->dtype == PB_F64 ? launch_stream_f64(h, sx.dev, count, bstride, st)
+                                : launch_stream_f32(h, sx.dev, count, bstride, st);
+    else if (h->shared() && h->plan.C > 0)
         rc = h->dtype == PB_F64
                  ? (h->K == 2 ? launch_tile_f64_k2(h, sx.dev, layout, count, bstride, st)
                               : launch_tile_f64_k1(h, sx.dev, layout, count, bstride, st))

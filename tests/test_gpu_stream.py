@@ -1,0 +1,105 @@
+"""GPU parity of the streaming two-phase solve (stream_solve.cuh): the
+interleaved shared-LHS path of pent_solve / tri_solve, at sizes that span one
+to 64 row tiles (R = 256), ragged tails in rows and in systems, cyclic and
+non-cyclic, fp64 (<= 1e-12) and fp32 (<= 1e-5 against the fp64 oracle)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2101_06550_b200 as pb  # noqa: E402
+
+
+@pytest.fixture(autouse=True)
+def _stream_path(monkeypatch):
+    """The streaming kernel is opt-in (PB_STREAM=1) while it is being tuned."""
+    monkeypatch.setenv("PB_STREAM", "1")
+
+TOL = {"f64": 1e-12, "f32": 1e-5}
+TDT = {"f64": torch.float64, "f32": torch.float32}
+
+
+def relerr(x, ref):
+    return float(np.max(np.abs(x - ref)) / max(np.max(np.abs(ref)), 1e-300))
+
+
+# (n, m): m keeps rows 16 B aligned for the TMA map (m % 4 == 0); n spans 1..64 tiles
+SIZES = [(64, 16), (256, 32), (257, 48), (600, 20), (1000, 64), (2500, 36), (5000, 32), (16384, 4)]
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("periodic", [False, True])
+@pytest.mark.parametrize("n,m", SIZES)
+def test_stream_penta(n, m, periodic, dtype):
+    a, b, c, d, e = synth.dd_penta(n, 1, seed=n)
+    f = synth.rhs_uniform(n, m, seed=m + 1)
+    ref = oracle.penta_batch_solve(a, b, c, d, e, f, n=n, m=m, periodic=periodic)
+    h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in (a, b, c, d, e)], batch=m, n=n, periodic=periodic,
+                       dtype=dtype)
+    x = torch.from_numpy(f).to(TDT[dtype]).cuda()
+    h.solve(x)
+    torch.cuda.synchronize()
+    assert relerr(x.double().cpu().numpy(), ref) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("periodic", [False, True])
+@pytest.mark.parametrize("n,m", SIZES)
+def test_stream_tri(n, m, periodic, dtype):
+    a, b, c = synth.dd_tri(n, 1, seed=n + 3)
+    f = synth.rhs_uniform(n, m, seed=m + 2)
+    ref = oracle.tri_batch_solve(a, b, c, f, n=n, m=m, periodic=periodic)
+    h = pb.tri_factor(*[torch.from_numpy(v).cuda() for v in (a, b, c)], batch=m, n=n, periodic=periodic, dtype=dtype)
+    x = torch.from_numpy(f).to(TDT[dtype]).cuda()
+    h.solve(x)
+    torch.cuda.synchronize()
+    assert relerr(x.double().cpu().numpy(), ref) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("n", [300, 2048, 8192])
+def test_stream_thesis_matrix(n, dtype):
+    """The thesis CH operator (sigma = 45.09, kappa = 722), cyclic: the bench matrix."""
+    m = 64
+    s_ = synth.SIGMA_STATS
+    diags = synth.const_penta(n, s_, -4 * s_, 1 + 6 * s_, -4 * s_, s_)
+    f = synth.rhs_uniform(n, m, seed=n)
+    ref = oracle.penta_batch_solve(*diags, f, n=n, m=m, periodic=True)
+    h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in diags], batch=m, n=n, periodic=True, dtype=dtype)
+    x = torch.from_numpy(f).to(TDT[dtype]).cuda()
+    h.solve(x)
+    torch.cuda.synchronize()
+    assert relerr(x.double().cpu().numpy(), ref) <= TOL[dtype]
+
+
+def test_stream_solve_many_and_repeat():
+    """count > 1 batches in one launch (3-D tensor map), and repeated launches
+    (per-call counters/flags start from zero every time)."""
+    n, m, cnt = 1100, 32, 3
+    a, b, c, d, e = synth.dd_penta(n, 1, seed=11)
+    f = synth.rhs_uniform(n, cnt * m, seed=12)
+    ref = np.concatenate([oracle.penta_batch_solve(a, b, c, d, e, f[k * n * m:(k + 1) * n * m], n=n, m=m,
+                                                   periodic=True) for k in range(cnt)])
+    h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in (a, b, c, d, e)], batch=m, n=n, periodic=True)
+    for _ in range(3):
+        x = torch.from_numpy(f).cuda()
+        h.solve_many(x, cnt, n * m)
+        torch.cuda.synchronize()
+        assert relerr(x.cpu().numpy(), ref) <= 1e-12
+
+
+def test_stream_matches_cluster_path(monkeypatch):
+    """The streaming path and the cluster path (PB_NO_STREAM) agree to rounding."""
+    n, m = 3000, 48
+    a, b, c, d, e = synth.dd_penta(n, 1, seed=21)
+    f = torch.from_numpy(synth.rhs_uniform(n, m, seed=22)).cuda()
+    h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in (a, b, c, d, e)], batch=m, n=n, periodic=True)
+    x1 = h.solve(f.clone())
+    monkeypatch.setenv("PB_NO_STREAM", "1")
+    x2 = h.solve(f.clone())
+    torch.cuda.synchronize()
+    assert float((x1 - x2).abs().max() / x2.abs().max()) <= 1e-13

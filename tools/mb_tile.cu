@@ -86,6 +86,14 @@ extern "C" int mb_run(int variant, const double *x, double *y, int64_t N, int64_
             case 9: launch<16, 256, 32, 2>(x, y, N, M, 0, st); break;
             case 10: launch<32, 1024, 16, 0>(x, y, N, M, 0, st); break;
             case 11: launch<8, 256, 32, 0>(x, y, N, M, 0, st); break;
+            case 12: launch<8, 256, 32, 2>(x, y, N, M, 0, st); break;
+            case 13: launch<4, 128, 32, 0>(x, y, N, M, 0, st); break;
+            case 14: launch<4, 128, 32, 2>(x, y, N, M, 0, st); break;
+            case 15: launch<8, 128, 32, 0>(x, y, N, M, 0, st); break;
+            case 16: launch<8, 128, 64, 2>(x, y, N, M, 0, st); break;
+            case 17: launch<4, 64, 64, 2>(x, y, N, M, 0, st); break;
+            case 18: launch<16, 256, 32, 0>(x, y, N, M, 0, st); break;
+            case 19: launch<32, 256, 32, 0>(x, y, N, M, 0, st); break;
             default: return -1;
         }
     }
@@ -95,4 +103,31 @@ extern "C" int mb_run(int variant, const double *x, double *y, int64_t N, int64_
     *ms /= reps;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : (int)e;
+}
+
+// dependent-chain latency probes: fp64 FMA, fp32 FMA (cycles per op)
+__global__ void lat_probe(double *out, float *outf, long long *cyc, int iters)
+{
+    double a = out[0], b = out[1], c = out[2];
+    float af = outf[0], bf = outf[1], cf = outf[2];
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) c = fma(a, c, b);
+    }
+    long long t1 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) cf = fmaf(af, cf, bf);
+    }
+    long long t2 = clock64();
+    out[3] = c;
+    outf[3] = cf;
+    cyc[0] = t1 - t0;
+    cyc[1] = t2 - t1;
+}
+extern "C" int mb_lat(double *out, float *outf, long long *cyc, int iters)
+{
+    lat_probe<<<1, 1>>>(out, outf, cyc, iters);
+    return (int)cudaDeviceSynchronize();
 }
