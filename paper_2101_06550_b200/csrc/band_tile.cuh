@@ -207,7 +207,8 @@ static int launch_tile_l(const Band *h, T *x, int layout, int64_t count, int64_t
 int const_penta_band(int64_t n, double sigma, int dtype, int cfg, int C, cudaStream_t st, Band **out);
 
 // streaming solve (stream_solve_f64.cu / _f32.cu): geometry per dtype and launchers
-constexpr int STREAM_R = 224;          // tile rows (PC * MR = 32 * 7) for both dtypes
+constexpr int STREAM_R = 256;          // max tile rows of the streaming solve (fp64 128, fp32 256)
+inline int stream_rows_per_tile(int dtype) { return dtype == PB_F64 ? 128 : 256; }
 constexpr int STREAM_MAX_NRB = 64;     // tiles per system the group scan supports
 int stream_build_tables(Band *h, cudaStream_t st);
 int launch_stream_f64(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st);

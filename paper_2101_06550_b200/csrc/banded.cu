@@ -395,45 +395,31 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
 int stream_build_tables(Band *h, cudaStream_t st)
 {
     const bool f64 = h->dtype == PB_F64;
-    const int PC = 32, MR = STREAM_R / PC;
-    const int R = STREAM_R;
+    const int R = stream_rows_per_tile(h->dtype);
     const int64_t nrb = (h->n + R - 1) / R;
     const int maxc = f64 ? stream_max_ctas_f64(h->K, h->periodic) : stream_max_ctas_f32(h->K, h->periodic);
     h->splan.ok = 0;
-    if (maxc <= 0 || nrb > maxc || nrb > STREAM_MAX_NRB || h->rows_alloc < nrb * R || !tensor_map_encoder()) return PB_OK;
+    if (maxc <= 0 || nrb > maxc || nrb > STREAM_MAX_NRB || h->rows_alloc < nrb * R || !tensor_map_encoder())
+        return PB_OK;
     const size_t es = dtype_size(h->dtype);
-    const int64_t nch = nrb * PC;
-    double *mfD = nullptr, *mbD = nullptr;
-    PB_CUDA_TRY(cudaMallocAsync(&mfD, sizeof(double) * 4 * nch, st));
-    PB_CUDA_TRY(cudaMallocAsync(&mbD, sizeof(double) * 4 * nch, st));
-    PB_CUDA_TRY(cudaMalloc(&h->splan.tab, es * TAB_STRIDE * nch));
     PB_CUDA_TRY(cudaMalloc(&h->splan.mft, es * 4 * nrb));
     PB_CUDA_TRY(cudaMalloc(&h->splan.mbt, es * 4 * nrb));
     PB_CUDA_TRY(cudaMalloc(&h->splan.hft, es * 4 * nrb));
     PB_CUDA_TRY(cudaMalloc(&h->splan.gsp, es * 8));
-    PB_CUDA_TRY(cudaMalloc(&h->splan.rsp, es * 4 * STREAM_R * nrb));
+    PB_CUDA_TRY(cudaMalloc(&h->splan.rsp, es * 4 * R * nrb));
     PB_CUDA_TRY(cudaMemsetAsync(h->splan.gsp, 0, es * 8, st));
-    const unsigned g = (unsigned)((nch + 127) / 128), gt = (unsigned)((nrb + 63) / 64);
-    transfer_kernel<<<g, 128, 0, st>>>(h->coefD, nch, MR, mfD, mbD);
-    PB_LAUNCH_CHECK();
-    if (f64) {
-        scan_table_kernel<double><<<g, 128, 0, st>>>(mfD, mbD, nch, PC, (double *)h->splan.tab);
-        PB_LAUNCH_CHECK();
+    const unsigned gt = (unsigned)((nrb + 63) / 64);
+    if (f64)
         tile_tables_kernel<double><<<gt, 64, 0, st>>>(h->coefD, (int)nrb, R, h->srow[0], h->srow[1], h->srow[2],
                                                       h->srow[3], (double *)h->splan.mft, (double *)h->splan.mbt,
                                                       (double *)h->splan.hft, (double *)h->splan.gsp,
                                                       (double *)h->splan.rsp);
-    } else {
-        scan_table_kernel<float><<<g, 128, 0, st>>>(mfD, mbD, nch, PC, (float *)h->splan.tab);
-        PB_LAUNCH_CHECK();
+    else
         tile_tables_kernel<float><<<gt, 64, 0, st>>>(h->coefD, (int)nrb, R, h->srow[0], h->srow[1], h->srow[2],
                                                      h->srow[3], (float *)h->splan.mft, (float *)h->splan.mbt,
                                                      (float *)h->splan.hft, (float *)h->splan.gsp,
                                                      (float *)h->splan.rsp);
-    }
     PB_LAUNCH_CHECK();
-    PB_CUDA_TRY(cudaFreeAsync(mfD, st));
-    PB_CUDA_TRY(cudaFreeAsync(mbD, st));
     for (int j = 0; j < 4; ++j) h->splan.srb[j] = h->srow[j] >= 0 ? (int)(h->srow[j] / R) : -1;
     h->splan.nrb = (int)nrb;
     h->splan.R = R;

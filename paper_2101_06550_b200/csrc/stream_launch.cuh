@@ -12,13 +12,13 @@ namespace pb {
 
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
 static_assert(MAX_NRB == STREAM_MAX_NRB, "group-scan capacity mismatch");
-static_assert(StreamSmem<double>::R == STREAM_R && StreamSmem<float>::R == STREAM_R, "tile rows");
+
 
 template <typename T, int K, bool PER>
 static int stream_prep(size_t *smem_out, int *blocks_per_sm)
 {
     auto kern = stream_solve_kernel<T, K, PER>;
-    const size_t smem = sizeof(StreamSmem<T>) + 1024;   // + alignment of the 1024-B swizzled slots
+    const size_t smem = sizeof(StreamSmem<T>) + 128;   // + alignment
     PB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     PB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, STREAM_THREADS, smem));
@@ -46,8 +46,7 @@ static int stream_max_ctas_t(int K, int periodic)
 template <typename T, int K, bool PER>
 static int launch_stream_t(const Band *h, T *x, int64_t count, int64_t bstride, cudaStream_t st)
 {
-    using G = StreamGeom<T>;
-    constexpr int W = G::W;
+    constexpr int W = StreamGeom<T>::W;
     auto kern = stream_solve_kernel<T, K, PER>;
     size_t smem;
     int occ;
@@ -69,12 +68,12 @@ static int launch_stream_t(const Band *h, T *x, int64_t count, int64_t bstride, 
         const int64_t bs = count > 1 ? bstride : M * n;
         cuuint64_t dims[3] = {(cuuint64_t)M, (cuuint64_t)n, (cuuint64_t)count};
         cuuint64_t strides[2] = {(cuuint64_t)(M * sizeof(T)), (cuuint64_t)(bs * sizeof(T))};
-        cuuint32_t box[3] = {(cuuint32_t)W, (cuuint32_t)STREAM_R, 1};
+        cuuint32_t box[3] = {(cuuint32_t)W, (cuuint32_t)StreamGeom<T>::R, 1};
         cuuint32_t es[3] = {1, 1, 1};
         auto enc = tensor_map_encoder();
         if (!enc) return set_error(PB_ECUDA, "cuTensorMapEncodeTiled unavailable");
         CUresult r = enc(&tmap, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
-                         (void *)x, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         (void *)x, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return set_error(PB_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     }

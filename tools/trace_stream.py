@@ -13,7 +13,7 @@ import synth  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 m = int(sys.argv[2]) if len(sys.argv) > 2 else n
-TEAMS = 3
+TEAMS = 8
 tr = torch.zeros(148 * TEAMS * 256 * 8, dtype=torch.int64, device="cuda")
 os.environ["PB_STREAM_TRACE"] = str(tr.data_ptr())
 import paper_2101_06550_b200 as pb  # noqa: E402
