@@ -22,6 +22,13 @@ struct StreamPlan {
     int srb[4] = {-1, -1, -1, -1};
 };
 
+// cluster solve plan (cluster_solve.cuh): chunk / CTA transfer matrices in dtype
+struct ClusterPlan {
+    int ok = 0, C = 0;
+    void *mf = nullptr, *mb = nullptr, *mfc = nullptr, *mbc = nullptr;
+    void *cc = nullptr;   // rows x 5 compact sweep coefficients (dtype)
+};
+
 struct Band {
     int K = 2;  // 2 = penta, 1 = tri
     int64_t batch = 0, n = 0, lhs_count = 1;
@@ -33,6 +40,7 @@ struct Band {
     double *scal = nullptr;   // SCAL_LEN
     Plan plan;
     StreamPlan splan;
+    ClusterPlan cplan;
     int64_t srow[4] = {-1, -1, -1, -1};
     // per-system LHS
     void *pcoef = nullptr;    // dtype, [(i*8 + j) * batch + s]
@@ -54,6 +62,11 @@ struct Band {
         cudaFree(splan.hft);
         cudaFree(splan.gsp);
         cudaFree(splan.rsp);
+        cudaFree(cplan.mf);
+        cudaFree(cplan.mb);
+        cudaFree(cplan.mfc);
+        cudaFree(cplan.mbc);
+        cudaFree(cplan.cc);
     }
 };
 
@@ -214,6 +227,12 @@ int stream_build_tables(Band *h, cudaStream_t st);
 int launch_stream_f64(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st);
 int launch_stream_f32(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st);
 int stream_max_ctas_f64(int K, int periodic);
+int cluster_build_tables(Band *h, cudaStream_t st);
+int launch_clu_f64(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st);
+int launch_clu_f32(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st);
+int clu_max_clusters_f64(int C, int K, int periodic);
+int clu_max_clusters_f32(int C, int K, int periodic);
+constexpr int CLU_RC = 512;   // rows per CTA of the cluster solve
 int stream_max_ctas_f32(int K, int periodic);
 
 // per-(dtype, K) entry points, defined in banded_inst_*.cu

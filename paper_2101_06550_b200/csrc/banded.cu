@@ -427,6 +427,70 @@ int stream_build_tables(Band *h, cudaStream_t st)
     return PB_OK;
 }
 
+// Plan of the cluster solve (cluster_solve.cuh): C = ceil(n / 512) CTAs per
+// group (<= 16), chunk transfer matrices (32 rows) and CTA block matrices.
+template <typename T>
+__global__ void compact_coef_kernel(const double *coef, int64_t rows, T *cc)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * 5; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / 5;
+        const int j = (int)(i % 5);
+        cc[i] = (T)coef[r * COEF_STRIDE + (j < 3 ? j : j + 1)];
+    }
+}
+
+__global__ void cast_f64_kernel(const double *src, float *dst, int64_t count)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = (float)src[i];
+}
+
+int cluster_build_tables(Band *h, cudaStream_t st)
+{
+    const bool f64 = h->dtype == PB_F64;
+    const int C = (int)((h->n + CLU_RC - 1) / CLU_RC);
+    h->cplan.ok = 0;
+    if (C > 16 || h->rows_alloc < (int64_t)C * CLU_RC || !tensor_map_encoder()) return PB_OK;
+    const int ncl = f64 ? clu_max_clusters_f64(C, h->K, h->periodic) : clu_max_clusters_f32(C, h->K, h->periodic);
+    if (ncl < 1) return PB_OK;
+    const size_t es = dtype_size(h->dtype);
+    const int64_t nch = (int64_t)C * (CLU_RC / 32);
+    double *mfD = nullptr, *mbD = nullptr;
+    PB_CUDA_TRY(cudaMallocAsync(&mfD, sizeof(double) * 4 * nch, st));
+    PB_CUDA_TRY(cudaMallocAsync(&mbD, sizeof(double) * 4 * nch, st));
+    PB_CUDA_TRY(cudaMalloc(&h->cplan.mf, es * 4 * nch));
+    PB_CUDA_TRY(cudaMalloc(&h->cplan.mb, es * 4 * nch));
+    PB_CUDA_TRY(cudaMalloc(&h->cplan.mfc, es * 4 * 16));
+    PB_CUDA_TRY(cudaMalloc(&h->cplan.mbc, es * 4 * 16));
+    PB_CUDA_TRY(cudaMalloc(&h->cplan.cc, es * 5 * (int64_t)C * CLU_RC));
+    if (f64)
+        compact_coef_kernel<double><<<64, 256, 0, st>>>(h->coefD, (int64_t)C * CLU_RC, (double *)h->cplan.cc);
+    else
+        compact_coef_kernel<float><<<64, 256, 0, st>>>(h->coefD, (int64_t)C * CLU_RC, (float *)h->cplan.cc);
+    PB_LAUNCH_CHECK();
+    transfer_kernel<<<(unsigned)((nch + 127) / 128), 128, 0, st>>>(h->coefD, nch, 32, mfD, mbD);
+    PB_LAUNCH_CHECK();
+    if (f64) {
+        PB_CUDA_TRY(cudaMemcpyAsync(h->cplan.mf, mfD, sizeof(double) * 4 * nch, cudaMemcpyDeviceToDevice, st));
+        PB_CUDA_TRY(cudaMemcpyAsync(h->cplan.mb, mbD, sizeof(double) * 4 * nch, cudaMemcpyDeviceToDevice, st));
+        block_transfer_kernel<double><<<1, 32, 0, st>>>(mfD, mbD, C, CLU_RC / 32, (double *)h->cplan.mfc,
+                                                       (double *)h->cplan.mbc);
+    } else {
+        cast_f64_kernel<<<16, 256, 0, st>>>(mfD, (float *)h->cplan.mf, 4 * nch);
+        PB_LAUNCH_CHECK();
+        cast_f64_kernel<<<16, 256, 0, st>>>(mbD, (float *)h->cplan.mb, 4 * nch);
+        PB_LAUNCH_CHECK();
+        block_transfer_kernel<float><<<1, 32, 0, st>>>(mfD, mbD, C, CLU_RC / 32, (float *)h->cplan.mfc,
+                                                      (float *)h->cplan.mbc);
+    }
+    PB_LAUNCH_CHECK();
+    PB_CUDA_TRY(cudaFreeAsync(mfD, st));
+    PB_CUDA_TRY(cudaFreeAsync(mbD, st));
+    h->cplan.C = C;
+    h->cplan.ok = 1;
+    return PB_OK;
+}
+
 // ---------------------------------------------------------------- one thread per system
 // The thesis's cuPentBatch kernel shape: g stored in place.
 // Used for per-system LHS and for shared LHS beyond the cluster capacity.
@@ -596,6 +660,8 @@ static int factor_impl(Band *h, const double *a, const double *b, const double *
         if (h->rows_alloc < n) h->rows_alloc = n;
         const int64_t stream_rows = (n + STREAM_R - 1) / STREAM_R * STREAM_R;
         if (h->rows_alloc < stream_rows) h->rows_alloc = stream_rows;
+        const int64_t clu_rows = (n + CLU_RC - 1) / CLU_RC * CLU_RC;
+        if (h->rows_alloc < clu_rows) h->rows_alloc = clu_rows;
         if (h->periodic) {
             if (h->K == 2) {
                 h->srow[0] = n - 4;
@@ -649,6 +715,7 @@ static int factor_impl(Band *h, const double *a, const double *b, const double *
             PB_CUDA_TRY(cudaFreeAsync(mbD, st));
         }
         if ((rc = stream_build_tables(h, st))) return rc;
+        if ((rc = cluster_build_tables(h, st))) return rc;
     } else {
         const int64_t M = h->batch;
         double *pcD = nullptr;
@@ -706,9 +773,19 @@ static int solve_impl(const Band *h, void *rhs, int layout, int64_t count, int64
     if (rc) return rc;
     sx.out_to(rhs);
     const bool al = (uintptr_t)sx.dev % 16 == 0 && (h->batch * es) % 16 == 0 && (count == 1 || (bstride * es) % 16 == 0);
-    if (h->shared() && layout == PB_INTERLEAVED && h->splan.ok && al && getenv("PB_STREAM") && !getenv("PB_NO_STREAM"))
+    // interleaved shared-LHS solver: the register-tile cluster kernel (default,
+    // fastest measured on B200 at the configs), the TMA cluster
+    // kernel (PB_SOLVER=cluster) or the streaming two-phase kernel (PB_SOLVER=stream)
+    const char *solver = getenv("PB_SOLVER");
+    const bool want_stream = (solver && !strcmp(solver, "stream")) || getenv("PB_STREAM");
+    const bool want_clu = solver && !strcmp(solver, "cluster");
+    const bool inter = h->shared() && layout == PB_INTERLEAVED && al;
+    if (inter && want_stream && h->splan.ok)
         rc = h->dtype == PB_F64 ? launch_stream_f64(h, sx.dev, count, bstride, st)
                                 : launch_stream_f32(h, sx.dev, count, bstride, st);
+    else if (inter && want_clu && h->cplan.ok)
+        rc = h->dtype == PB_F64 ? launch_clu_f64(h, sx.dev, count, bstride, st)
+                                : launch_clu_f32(h, sx.dev, count, bstride, st);
     else if (h->shared() && h->plan.C > 0)
         rc = h->dtype == PB_F64
                  ? (h->K == 2 ? launch_tile_f64_k2(h, sx.dev, layout, count, bstride, st)

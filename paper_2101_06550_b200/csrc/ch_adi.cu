@@ -225,23 +225,40 @@ static int launch_adi_cfg(const Band *h, const AdiArgs<T> &A, int64_t sims, cuda
 // Tile configuration for a sweep of length n: the smallest per-CTA row span
 // that covers n (one CTA per system group), else the largest span with a
 // cluster of ceil(n / span) CTAs (<= 16).
+// shared memory of pass A (the larger pass) for tile configuration k
+static size_t adi_smem(int k, int dtype)
+{
+    const TileCfg *T = dtype == PB_F64 ? CFG64 : CFG32;
+    const int W = dtype == PB_F64 ? 16 : 32;
+    const size_t es = dtype == PB_F64 ? 8 : 4;
+    const size_t RC = (size_t)(T[k].nt / W) * T[k].mr, PC = T[k].nt / W;
+    const size_t dyn = es * (RC * COEF_STRIDE + RC * (W + 1) + (W + 4) * (ADI_IB + 4) + (W + 2) * (ADI_IB + 2) + W * ADI_IB);
+    const size_t stat = es * (4 * W * (PC + 1) + 2 * MAX_CLUSTER * W * 2 + 4 * W + 2 * W);
+    return dyn + stat;
+}
+
 static int adi_choose(int64_t n, int dtype, int *C)
 {
     const TileCfg *T = dtype == PB_F64 ? CFG64 : CFG32;
     const int W = dtype == PB_F64 ? 16 : 32;
+    const size_t limit = 227 * 1024;
     for (int k = 0; k < NCFG; ++k) {
         int64_t rc = (int64_t)(T[k].nt / W) * T[k].mr;
-        if (rc >= n) {
+        if (rc >= n && adi_smem(k, dtype) <= limit) {
             *C = 1;
             return k;
         }
     }
-    int k = NCFG - 1;
-    int64_t rc = (int64_t)(T[k].nt / W) * T[k].mr;
-    int64_t c = (n + rc - 1) / rc;
-    if (c > MAX_CLUSTER) return -1;
-    *C = (int)c;
-    return k;
+    // multi-CTA cluster: the largest row span whose pass A fits in shared memory
+    for (int k = NCFG - 1; k >= 0; --k) {
+        if (adi_smem(k, dtype) > limit) continue;
+        int64_t rc = (int64_t)(T[k].nt / W) * T[k].mr;
+        int64_t c = (n + rc - 1) / rc;
+        if (c > MAX_CLUSTER) return -1;
+        *C = (int)c;
+        return k;
+    }
+    return -1;
 }
 
 static std::mutex g_adi_mu;
