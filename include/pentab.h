@@ -179,6 +179,34 @@ PB_API int ch_workspace_bytes(int64_t sims, int64_t n, int dtype, size_t *bytes)
 PB_API int ch_adi_step(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nsteps, void *stream);
 
 /* ------------------------------------------------------------------------
+ * Row-partitioned ADI step (configs[4]: one n x n grid over P ranks,
+ * SURVEY §8(e)).  Rank r owns rows [r n/P, (r+1) n/P); one step of Eq 3.1
+ * is, per rank (the orchestration and the two all-to-all
+ * transposes live in paper_2101_06550_b200/dist.py):
+ *   halo rows -> ch_dist_pass_a (RHS + x-sweep) -> ch_dist_pack ->
+ *   all-to-all -> pent_solve (y-sweep on the rank's n/P columns, interleaved)
+ *   -> all-to-all -> ch_dist_combine (C^{n+1} = 2C^n - C^{n-1} + v).
+ * The x-then-y order is the thesis's (reading r18); results equal the
+ * single-grid ch_adi_step up to rounding.
+ *
+ * ch_dist_pass_a: cn_ext, cm_ext: device, (rows + 4) x n, rows 2..rows+1 the
+ *   rank's rows, rows 0-1 / rows+2..rows+3 the two halo rows of the previous /
+ *   next rank (periodic in j across ranks, periodic in i within the row).
+ *   w: device rows x n, receives L_x^{-1} R.  dt, p as ch_adi_step.
+ * ch_dist_pack: w (rows x n) -> packed [parts][rows][n/parts] (the send layout
+ *   of the transpose: column block q contiguous).  n % parts == 0.
+ * ch_dist_combine: cm_ext interior rows <- 2 cn_ext - cm_ext + v, with v in
+ *   the receive layout [parts][rows][n/parts] (block q = columns of rank q).
+ * All buffers are caller-owned device memory; work is enqueued on stream.
+ * Errors: PB_EINVAL (sizes, pointers, dtype), PB_ECUDA.                    */
+PB_API int ch_dist_pass_a(int64_t rows, int64_t n, int dtype, const void *cn_ext, const void *cm_ext, void *w,
+                          double dt, const pb_ch_params *p, void *stream);
+PB_API int ch_dist_pack(int64_t rows, int64_t n, int64_t parts, int dtype, const void *w, void *packed,
+                        void *stream);
+PB_API int ch_dist_combine(int64_t rows, int64_t n, int64_t parts, int dtype, const void *cn_ext, void *cm_ext,
+                           const void *v_packed, void *stream);
+
+/* ------------------------------------------------------------------------
  * diagnostics */
 /* Last error of the calling thread: code, system/row of a pivot failure,
  * message (NUL-terminated, truncated to len).  Returns the code.          */

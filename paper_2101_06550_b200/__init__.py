@@ -22,8 +22,9 @@ PB_NONPERIODIC, PB_PERIODIC = 0, 1
 
 # every symbol include/pentab.h declares
 EXPORTS = ("pent_factor", "pent_solve", "pent_solve_many", "pent_destroy", "tri_factor", "tri_solve",
-           "tri_destroy", "stencil_apply", "ch_workspace_bytes", "ch_adi_step", "pb_last_error",
-           "pb_launch_count", "pb_reset_launch_count", "pb_device_ok")
+           "tri_destroy", "stencil_apply", "ch_workspace_bytes", "ch_adi_step", "ch_dist_pass_a",
+           "ch_dist_pack", "ch_dist_combine", "pb_last_error", "pb_launch_count", "pb_reset_launch_count",
+           "pb_device_ok")
 
 
 class PentabError(RuntimeError):
@@ -70,6 +71,9 @@ def lib() -> ctypes.CDLL:
         L.stencil_apply.argtypes = [ctypes.POINTER(pb_grid), P, P, ctypes.POINTER(pb_window), P, I, P]
         L.ch_workspace_bytes.argtypes = [I64, I64, I, ctypes.POINTER(ctypes.c_size_t)]
         L.ch_adi_step.argtypes = [ctypes.POINTER(pb_ch_state), D, ctypes.POINTER(pb_ch_params), I64, P]
+        L.ch_dist_pass_a.argtypes = [I64, I64, I, P, P, P, D, ctypes.POINTER(pb_ch_params), P]
+        L.ch_dist_pack.argtypes = [I64, I64, I64, I, P, P, P]
+        L.ch_dist_combine.argtypes = [I64, I64, I64, I, P, P, P, P]
         L.pb_last_error.argtypes = [ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.c_char_p, ctypes.c_size_t]
         L.pb_launch_count.restype = I64
         L.pb_reset_launch_count.restype = None
@@ -246,3 +250,20 @@ def reset_launch_count():
 
 def device_ok() -> bool:
     return lib().pb_device_ok() == PB_OK
+
+
+# ---------------------------------------------------------------- row-partitioned ADI (configs[4])
+def ch_dist_pass_a(cn_ext, cm_ext, w, *, rows, n, dt, D=1.0, gamma=0.01, L, stream=None):
+    """RHS + x-sweep of a row block with 2 halo rows each side (pentab.h)."""
+    p = pb_ch_params(D, gamma, L)
+    _check(lib().ch_dist_pass_a(rows, n, _dtype_code(w), _ptr(cn_ext), _ptr(cm_ext), _ptr(w), dt, ctypes.byref(p),
+                                _stream(w, stream)))
+
+
+def ch_dist_pack(w, packed, *, rows, n, parts, stream=None):
+    _check(lib().ch_dist_pack(rows, n, parts, _dtype_code(w), _ptr(w), _ptr(packed), _stream(w, stream)))
+
+
+def ch_dist_combine(cn_ext, cm_ext, v_packed, *, rows, n, parts, stream=None):
+    _check(lib().ch_dist_combine(rows, n, parts, _dtype_code(cn_ext), _ptr(cn_ext), _ptr(cm_ext), _ptr(v_packed),
+                                 _stream(cn_ext, stream)))

@@ -20,6 +20,8 @@
 // grad^4 = dx^4 + 2 dx^2 dy^2 + dy^4 with the Fig 3.1 cross stencil (r9).
 #include <string.h>
 
+#include <algorithm>
+
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -36,6 +38,10 @@ struct AdiArgs {
     T *w;
     int64_t n;
     T k_dif, k_bih, k_lap;  // R = k_dif (C^n - C^{n-1}) + k_bih BIH(Cbar) + k_lap LAP(C^3 - C)
+    // row-partitioned grids (ch_dist_pass_a): `rows` local rows; cn / cm hold
+    // rows + 4 rows (2 halo rows above and below, no wrap in j); w holds `rows`
+    int64_t rows = 0;
+    int ext = 0;
 };
 
 constexpr int ADI_IB = 32;  // stencil column block
@@ -47,15 +53,16 @@ __device__ __forceinline__ int64_t wrapi(int64_t x, int64_t n)
     return x;
 }
 
-template <typename T, int W, int NT, int MR>
+template <typename T, int W, int NT, int MR, bool EXT = false>
 __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) adi_pass_a(const AdiArgs<T> A)
 {
     constexpr int PC = NT / W, RC = PC * MR, WP = W + 1, IB = ADI_IB;
     constexpr int SB = IB + 4, SN = IB + 2;  // staged row strides (Cbar halo 2, NL halo 1)
     __shared__ CoreSmem<T, W, PC> S;
     extern __shared__ __align__(16) unsigned char dyn_smem[];
-    T *cs = reinterpret_cast<T *>(dyn_smem);    // [RC][8] coefficient rows of this CTA
-    T *tile = cs + RC * COEF_STRIDE;             // [RC][W+1]: R, then w
+    // coefficient rows are read through L1 here (not staged): pass A's shared
+    // memory (solve tile + stencil staging) then allows two CTAs per SM
+    T *tile = reinterpret_cast<T *>(dyn_smem);   // [RC][W+1]: R, then w
     T *cb = tile + RC * WP;                      // [W+4][IB+4] Cbar
     T *nl = cb + (W + 4) * SB;                   // [W+2][IB+2] C^3 - C
     T *dl = nl + (W + 2) * SN;                   // [W][IB]     C^n - C^{n-1}
@@ -63,12 +70,13 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) adi_pass_a(const AdiA
     const int C = A.core.C;
     const int c = (C > 1) ? (int)cg::this_cluster().block_rank() : 0;
     const int64_t n = A.n, j0 = (int64_t)(blockIdx.x / C) * W;
-    const int64_t plane = n * n;
-    const T *Cn = A.cn + (int64_t)blockIdx.y * plane;
-    const T *Cm = A.cm + (int64_t)blockIdx.y * plane;
-    T *Wo = A.w + (int64_t)blockIdx.y * plane;
+    const int64_t rows = EXT ? A.rows : n;
+    const int64_t plane_in = (EXT ? rows + 4 : n) * n, plane_w = rows * n;
+    const T *Cn = A.cn + (int64_t)blockIdx.y * plane_in;
+    const T *Cm = A.cm + (int64_t)blockIdx.y * plane_in;
+    T *Wo = A.w + (int64_t)blockIdx.y * plane_w;
     const int64_t ib0 = (int64_t)c * RC;  // first solve row (grid column i) of this CTA
-    stage_coef<T, NT>(cs, A.core.coef + ib0 * COEF_STRIDE, RC);
+    const T *cs = A.core.coef + ib0 * COEF_STRIDE;
 
     // ---- stencil RHS into the solve tile, column block by column block
     for (int ib = 0; ib < RC; ib += IB) {
@@ -77,7 +85,9 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) adi_pass_a(const AdiA
         if (live) {
             for (int e = tid; e < (W + 4) * SB; e += NT) {
                 const int r = e / SB, q = e % SB;
-                const int64_t idx = wrapi(j0 - 2 + r, n) * n + wrapi(i0 - 2 + q, n);
+                // periodic in j (whole grid), or halo rows of a row block (ext)
+                const int64_t jr = EXT ? (j0 + r < rows + 3 ? j0 + r : rows + 3) : wrapi(j0 - 2 + r, n);
+                const int64_t idx = jr * n + wrapi(i0 - 2 + q, n);
                 const T cnv = __ldg(Cn + idx), cmv = __ldg(Cm + idx);
                 cb[e] = T(2) * cnv - cmv;
                 if (r >= 1 && r < W + 3 && q >= 1 && q < IB + 3) nl[(r - 1) * SN + (q - 1)] = cnv * cnv * cnv - cnv;
@@ -114,7 +124,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) adi_pass_a(const AdiA
     for (int e = tid; e < W * RC; e += NT) {
         const int jj = e / RC, ii = e % RC;
         const int64_t j = j0 + jj, i = ib0 + ii;
-        if (j < n && i < n) __stcg(Wo + j * n + i, tile[ii * WP + jj]);
+        if (j < rows && i < n) __stcg(Wo + j * n + i, tile[ii * WP + jj]);
     }
 }
 
@@ -166,7 +176,7 @@ static int launch_adi(const Band *h, const AdiArgs<T> &A, int64_t sims, cudaStre
 {
     constexpr int PC = NT / W, RC = PC * MR;
     const int C = h->plan.C;
-    const int64_t groups = (A.n + W - 1) / W;
+    const int64_t groups = ((A.ext ? A.rows : A.n) + W - 1) / W;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(groups * C), (unsigned)sims, 1);
     cfg.blockDim = dim3(NT, 1, 1);
@@ -179,8 +189,8 @@ static int launch_adi(const Band *h, const AdiArgs<T> &A, int64_t sims, cudaStre
     cfg.attrs = at;
     cfg.numAttrs = C > 1 ? 1 : 0;
     if (pass_a) {
-        auto kern = adi_pass_a<T, W, NT, MR>;
-        const size_t dyn = sizeof(T) * ((size_t)RC * COEF_STRIDE + (size_t)RC * (W + 1) + (W + 4) * (ADI_IB + 4) +
+        auto kern = A.ext ? adi_pass_a<T, W, NT, MR, true> : adi_pass_a<T, W, NT, MR, false>;
+        const size_t dyn = sizeof(T) * ((size_t)RC * (W + 1) + (W + 4) * (ADI_IB + 4) +
                                         (W + 2) * (ADI_IB + 2) + W * ADI_IB);
         int rc = prep_kernel(kern, dyn, C);
         if (rc) return rc;
@@ -232,7 +242,7 @@ static size_t adi_smem(int k, int dtype)
     const int W = dtype == PB_F64 ? 16 : 32;
     const size_t es = dtype == PB_F64 ? 8 : 4;
     const size_t RC = (size_t)(T[k].nt / W) * T[k].mr, PC = T[k].nt / W;
-    const size_t dyn = es * (RC * COEF_STRIDE + RC * (W + 1) + (W + 4) * (ADI_IB + 4) + (W + 2) * (ADI_IB + 2) + W * ADI_IB);
+    const size_t dyn = es * (RC * (W + 1) + (W + 4) * (ADI_IB + 4) + (W + 2) * (ADI_IB + 2) + W * ADI_IB);
     const size_t stat = es * (4 * W * (PC + 1) + 2 * MAX_CLUSTER * W * 2 + 4 * W + 2 * W);
     return dyn + stat;
 }
@@ -324,6 +334,116 @@ static int adi_run(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nst
 }
 
 }  // namespace pb
+
+namespace pb {
+
+// w [rows][n] -> packed [parts][rows][nb]: column block q becomes a contiguous
+// [rows][nb] slab, the send layout of the all-to-all transpose.
+template <typename T>
+__global__ void dist_pack_kernel(int64_t rows, int64_t n, int64_t parts, const T *w, T *out)
+{
+    const int64_t nb = n / parts, total = rows * n;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = e / n, i = e % n, q = i / nb, ii = i % nb;
+        out[(q * rows + j) * nb + ii] = w[e];
+    }
+}
+
+// C^{n+1} = 2 C^n - C^{n-1} + v on the interior rows of a row block (written
+// over C^{n-1}); v arrives as [parts][rows][nb] (block q = columns of rank q).
+template <typename T>
+__global__ void dist_combine_kernel(int64_t rows, int64_t n, int64_t parts, const T *cn, T *cm, const T *v)
+{
+    const int64_t nb = n / parts, total = rows * n;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = e / n, i = e % n, q = i / nb, ii = i % nb;
+        const int64_t x = (j + 2) * n + i;
+        cm[x] = (T(2) * cn[x] - cm[x]) + v[(q * rows + j) * nb + ii];
+    }
+}
+
+template <typename T>
+static int dist_pass_a(int64_t rows, int64_t n, const void *cn, const void *cm, void *w, double dt,
+                       const pb_ch_params *p, cudaStream_t st)
+{
+    const double dx = p->L / (double)n;  // r1
+    const double sigma = (2.0 / 3.0) * p->D * p->gamma * dt / (dx * dx * dx * dx);
+    Band *h = nullptr;
+    int rc = adi_band(n, sigma, sizeof(T) == 8 ? PB_F64 : PB_F32, st, &h);
+    if (rc) return rc;
+    AdiArgs<T> A;
+    A.core.coef = (const T *)h->coef;
+    A.core.tab = (const T *)h->plan.tab;
+    A.core.mfc = (const T *)h->plan.mfc;
+    A.core.mbc = (const T *)h->plan.mbc;
+    A.core.scal = h->scal;
+    A.core.n = n;
+    A.core.C = h->plan.C;
+    for (int j = 0; j < 4; ++j) A.core.srow[j] = h->srow[j];
+    A.n = n;
+    A.k_dif = T(-2.0 / 3.0);
+    A.k_bih = T(-(2.0 / 3.0) * dt * p->D * p->gamma / (dx * dx * dx * dx));
+    A.k_lap = T((2.0 / 3.0) * p->D * dt / (dx * dx));
+    A.cn = (const T *)cn;
+    A.cm = (T *)cm;
+    A.w = (T *)w;
+    A.rows = rows;
+    A.ext = 1;
+    return launch_adi_cfg<T>(h, A, 1, st, true);
+}
+
+}  // namespace pb
+
+extern "C" int ch_dist_pass_a(int64_t rows, int64_t n, int dtype, const void *cn_ext, const void *cm_ext, void *w,
+                              double dt, const pb_ch_params *p, void *stream)
+{
+    using namespace pb;
+    if (!p || !cn_ext || !cm_ext || !w || rows < 1 || n < 8 || rows > n) return set_error(PB_EINVAL, "bad args");
+    if (dtype != PB_F64 && dtype != PB_F32) return set_error(PB_EINVAL, "bad dtype");
+    if (!(dt > 0) || !(p->L > 0)) return set_error(PB_EINVAL, "dt and L must be positive");
+    if (pb_device_ok() != PB_OK) return PB_ECUDA;
+    if (!is_device_ptr(cn_ext) || !is_device_ptr(cm_ext) || !is_device_ptr(w))
+        return set_error(PB_EINVAL, "ch_dist_pass_a buffers must be device memory");
+    cudaStream_t st = (cudaStream_t)stream;
+    return dtype == PB_F64 ? dist_pass_a<double>(rows, n, cn_ext, cm_ext, w, dt, p, st)
+                           : dist_pass_a<float>(rows, n, cn_ext, cm_ext, w, dt, p, st);
+}
+
+extern "C" int ch_dist_pack(int64_t rows, int64_t n, int64_t parts, int dtype, const void *w, void *packed,
+                            void *stream)
+{
+    using namespace pb;
+    if (!w || !packed || rows < 1 || parts < 1 || n % parts) return set_error(PB_EINVAL, "bad args");
+    if (dtype != PB_F64 && dtype != PB_F32) return set_error(PB_EINVAL, "bad dtype");
+    if (pb_device_ok() != PB_OK) return PB_ECUDA;
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned g = (unsigned)std::min<int64_t>((rows * n + 255) / 256, 148 * 16);
+    if (dtype == PB_F64)
+        dist_pack_kernel<double><<<g, 256, 0, st>>>(rows, n, parts, (const double *)w, (double *)packed);
+    else
+        dist_pack_kernel<float><<<g, 256, 0, st>>>(rows, n, parts, (const float *)w, (float *)packed);
+    PB_LAUNCH_CHECK();
+    return PB_OK;
+}
+
+extern "C" int ch_dist_combine(int64_t rows, int64_t n, int64_t parts, int dtype, const void *cn_ext, void *cm_ext,
+                               const void *v_packed, void *stream)
+{
+    using namespace pb;
+    if (!cn_ext || !cm_ext || !v_packed || rows < 1 || parts < 1 || n % parts) return set_error(PB_EINVAL, "bad args");
+    if (dtype != PB_F64 && dtype != PB_F32) return set_error(PB_EINVAL, "bad dtype");
+    if (pb_device_ok() != PB_OK) return PB_ECUDA;
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned g = (unsigned)std::min<int64_t>((rows * n + 255) / 256, 148 * 16);
+    if (dtype == PB_F64)
+        dist_combine_kernel<double><<<g, 256, 0, st>>>(rows, n, parts, (const double *)cn_ext, (double *)cm_ext,
+                                                       (const double *)v_packed);
+    else
+        dist_combine_kernel<float><<<g, 256, 0, st>>>(rows, n, parts, (const float *)cn_ext, (float *)cm_ext,
+                                                      (const float *)v_packed);
+    PB_LAUNCH_CHECK();
+    return PB_OK;
+}
 
 extern "C" int ch_workspace_bytes(int64_t sims, int64_t n, int dtype, size_t *bytes)
 {
