@@ -354,6 +354,49 @@ def bench_adi(args, rank, world, dev):
     }
 
 
+DIST_N = 16384                     # configs[4]: one 16384^2 grid over the ranks
+DIST_L = DIST_N * synth.DX_STATS   # 128 pi: dx = 2 pi / 256
+
+
+def bench_dist_adi(args, rank, world, dev):
+    """configs[4]: one 16384^2 CH grid row-partitioned over the ranks, two
+    all-to-all transposes per step (paper_2101_06550_b200.dist, NCCL).
+    Time-steps/s of the whole grid; max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2101_06550_b200 import dist as pdist
+
+    n = args.dist_n
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    dt = synth.ch_dt(n, n * synth.DX_STATS)
+    prm = pdist.Params(n=n, parts=world, dt=dt, L=n * synth.DX_STATS)
+    g = torch.Generator(device=dev)
+    g.manual_seed(5 + rank)   # IC U(-0.1, 0.1), this rank's rows (synthetic)
+    rows = torch.empty((prm.rows, n), dtype=tdt, device=dev).uniform_(-0.1, 0.1, generator=g)
+    st = pdist.RankState(prm, rank, rows, rows, pdist.LibCompute(prm, dev, tdt))
+    del rows
+    ex = pdist.TorchExchange() if world > 1 else pdist.LocalExchange()
+    for _ in range(max(args.warmup, 1)):
+        pdist.step([st], ex)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    steps = args.dist_steps
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        pdist.step([st], ex)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = max_over_ranks(e0.elapsed_time(e1), dev)
+    es = 8 if args.dtype == "f64" else 4
+    a2a = 2 * es * prm.rows * n * (world - 1) / world   # bytes each rank sends per step (two transposes)
+    return {"value": round(steps / (ms * 1e-3), 3), "unit": "grid-timesteps/s", "ms_per_step": ms / steps,
+            "steps": steps, "config": {"workload": f"configs[4]: one {n}^2 CH grid, L=128pi, row-partitioned x{world}",
+                                       "exchange": "2 all-to-all transposes + halo rows per step (torch.distributed)"},
+            "a2a_bytes_per_rank_per_step": a2a}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -374,6 +417,12 @@ def run_ours(args):
     pb.lib()
     r = bench_penta(args, rank, world, dev)
     adi = bench_adi(args, rank, world, dev) if not args.no_adi else None
+    dist_adi = None
+    if (world > 1 or args.dist_force) and not args.no_dist:
+        try:
+            dist_adi = bench_dist_adi(args, rank, world, dev)
+        except Exception as ex:  # reported, never fatal to the headline
+            dist_adi = {"error": f"{type(ex).__name__}: {ex}"[:300]}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, sample = oracle_penta_sample(args.cpu_budget)
@@ -391,7 +440,7 @@ def run_ours(args):
                        "layout": "interleaved", "l2": "inputs (512 MiB fp64) larger than the 126 MB L2; no flush",
                        "parallelism": f"independent batches x{world}"},
             "roofline": r["roofline"], "cpu_baseline": cpu, "e2e": r["e2e"], "gpu_launches": r["launches"],
-            "clocks": r["clocks"], "residual": r["residual"], "ch_adi": adi,
+            "clocks": r["clocks"], "residual": r["residual"], "ch_adi": adi, "dist_adi": dist_adi,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -442,6 +491,10 @@ def main(argv=None):
     ap.add_argument("--dtype", choices=["f64", "f32"], default="f64")
     ap.add_argument("--no-adi", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-dist", action="store_true", help="skip the configs[4] row-partitioned leg (N > 1)")
+    ap.add_argument("--dist-n", type=int, default=DIST_N)
+    ap.add_argument("--dist-steps", type=int, default=20)
+    ap.add_argument("--dist-force", action="store_true", help="run the configs[4] leg at N = 1 too (one rank)")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     args = ap.parse_args(argv)
     if args.warmup < 3:
