@@ -48,24 +48,20 @@ __host__ __device__ constexpr int W_OF() { return Geom<T>::W; }
 template <typename T>
 struct Smem {
     static constexpr int W = Geom<T>::W;
+    static constexpr int PAIRS = PC / 2;
     T buf[NB][RC * W];          // group buffers (TMA destination / source)
+    // coefficient rows of this CTA, chunk pairs interleaved: the two chunks a
+    // fp64 warp spans read adjacent 16-byte words (one wavefront per load)
+    T cF[MR][PAIRS][2][2];      // (F0, F1) of row k of chunk 2w+h
+    T cB[MR][PAIRS][2][2];      // (B1, B2)
+    T cF2[MR][PAIRS][2];        // F2
     T cf[PC][W][2];             // chunk carries
-    T red[PC][W][2];            // aggregate partial sums
-    T agg[W][2];                // this CTA's aggregate (to the peers)
+    T agg[W][2];                // this CTA's aggregate (to the peers); later the cyclic pair x_l
     T aggF[MAXC][W][2];         // exchange 1: CTA forward aggregates (written by peers)
     T aggB[MAXC][W][2];         // exchange 2: CTA backward aggregates
     T spec[4][W];               // exchange 2: forward values on the cyclic rows (from their owner)
-    T xl[W][2];                 // cyclic pair
     T mf[PC][4], mb[PC][4];     // chunk transfer matrices
     T mfc[MAXC][4], mbc[MAXC][4];   // CTA block transfer matrices
-    // products of transfer matrices (prologue): chunk level
-    T phi[PC][4];               // Mf_{p-1} .. Mf_0        (CTA inflow -> chunk p inflow)
-    T sfx[PC][4];               // Mf_15 .. Mf_{q+1}       (chunk q carry -> CTA aggregate)
-    T psi[PC][4];               // Mb_{p+1} .. Mb_15       (backward)
-    T sbx[PC][4];               // Mb_0 .. Mb_{q-1}
-    // CTA level, for this CTA c
-    T pcf[MAXC][4];             // Mfc_{c-1} .. Mfc_{c'+1}  (aggF of c' < c -> inflow of c)
-    T pcb[MAXC][4];             // Mbc_{c+1} .. Mbc_{c'-1}  (aggB of c' > c -> inflow of c)
     uint64_t full[NB], empty[NB];
     uint64_t xf, xb;            // exchange barriers (C remote arrivals each)
 };
@@ -287,6 +283,29 @@ __device__ __forceinline__ void mm(const T *a, const T *b, T *r)
 template <typename T>
 __device__ __forceinline__ void set_id(T *r) { r[0] = T(1), r[1] = T(0), r[2] = T(0), r[3] = T(1); }
 
+// shared loads the compiler keeps in program order (bounds the register
+// footprint of the coefficient prefetch in the fully unrolled sweeps)
+__device__ __forceinline__ void lds2(const double *p, double &a, double &b)
+{
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(su32(p)));
+}
+__device__ __forceinline__ void lds2(const float *p, float &a, float &b)
+{
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(a), "=f"(b) : "r"(su32(p)));
+}
+__device__ __forceinline__ double lds1(const double *p)
+{
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(su32(p)));
+    return v;
+}
+__device__ __forceinline__ float lds1(const float *p)
+{
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(su32(p)));
+    return v;
+}
+
 template <typename T, int K, bool PER>
 __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                            const Args<T> A)
@@ -313,6 +332,15 @@ __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(cons
         bar_init(&sm.xb, C);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    for (int e = tid; e < RC; e += blockDim.x) {
+        const int pp = e / MR, k = e % MR, w = pp / 2, h = pp % 2;
+        const T *cr = A.coef + (row0 + e) * COEF_STRIDE;
+        sm.cF[k][w][h][0] = cr[0];
+        sm.cF[k][w][h][1] = cr[1];
+        sm.cF2[k][w][h] = cr[2];
+        sm.cB[k][w][h][0] = cr[4];
+        sm.cB[k][w][h][1] = cr[5];
+    }
     for (int e = tid; e < PC * 4; e += blockDim.x) {
         sm.mf[e / 4][e % 4] = A.mf[((int64_t)c * PC) * 4 + e];
         sm.mb[e / 4][e % 4] = A.mb[((int64_t)c * PC) * 4 + e];
@@ -320,45 +348,6 @@ __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(cons
     for (int e = tid; e < C * 4; e += blockDim.x) {
         sm.mfc[e / 4][e % 4] = A.mfc[e];
         sm.mbc[e / 4][e % 4] = A.mbc[e];
-    }
-    __syncthreads();
-    // transfer-matrix products (LHS-only, once per kernel)
-    if (tid == 0) {
-        T m[4];
-        set_id(m);
-        for (int p = 0; p < PC; ++p) {   // phi_p = Mf_{p-1} .. Mf_0
-            for (int j = 0; j < 4; ++j) sm.phi[p][j] = m[j];
-            mm(sm.mf[p], m, m);
-        }
-        set_id(m);
-        for (int q = PC - 1; q >= 0; --q) {   // sfx_q = Mf_15 .. Mf_{q+1}
-            for (int j = 0; j < 4; ++j) sm.sfx[q][j] = m[j];
-            mm(m, sm.mf[q], m);
-        }
-    } else if (tid == 32) {
-        T m[4];
-        set_id(m);
-        for (int p = PC - 1; p >= 0; --p) {   // psi_p = Mb_{p+1} .. Mb_15
-            for (int j = 0; j < 4; ++j) sm.psi[p][j] = m[j];
-            mm(sm.mb[p], m, m);
-        }
-        set_id(m);
-        for (int q = 0; q < PC; ++q) {   // sbx_q = Mb_0 .. Mb_{q-1}
-            for (int j = 0; j < 4; ++j) sm.sbx[q][j] = m[j];
-            mm(m, sm.mb[q], m);
-        }
-    } else if (tid == 64) {
-        T m[4];
-        set_id(m);
-        for (int cc = (int)c - 1; cc >= 0; --cc) {   // pcf[c'] = Mfc_{c-1} .. Mfc_{c'+1}
-            for (int j = 0; j < 4; ++j) sm.pcf[cc][j] = m[j];
-            mm(m, sm.mfc[cc], m);
-        }
-        set_id(m);
-        for (int cc = (int)c + 1; cc < C; ++cc) {   // pcb[c'] = Mbc_{c+1} .. Mbc_{c'-1}
-            for (int j = 0; j < 4; ++j) sm.pcb[cc][j] = m[j];
-            mm(m, sm.mbc[cc], m);
-        }
     }
     __syncthreads();
     if (C > 1) cg::this_cluster().sync();   // peers' barriers initialised before any remote arrive
@@ -386,82 +375,103 @@ __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(cons
 
     // ================= consumers: thread = (chunk p, system s); its 32 values live in registers
     const int s = tid % W, p = tid / W;
+    const int pw = p / 2, ph2 = p % 2;                 // coefficient pair slot
     const int k0 = p * MR;                             // first row of the chunk in the CTA
-    const T *ccr = A.coef + (row0 + k0) * COEF_STRIDE;   // coefficient rows of the chunk (L1-resident)
     int pend = -1;                                     // buffer whose TMA store is pending
     for (int t = 0; t < ng; ++t) {
         const int b = t % NB;
         const uint32_t ph = t & 1;
+        CLU_TR(0);
         bar_wait(&sm.full[b], (t / NB) & 1);
+        CLU_TR(1);
         T *col = sm.buf[b] + s + k0 * W;   // row k of the chunk at col[k * W]
+        T v[MR];
+#pragma unroll
+        for (int k = 0; k < MR; ++k) v[k] = col[k * W];
 
-        // ---- sweep 1: forward, zero inflow -> chunk carry; its share of the CTA aggregate
+        // ---- sweep 1: forward, zero inflow -> chunk carry
         {
             T y0 = T(0), y1 = T(0);
-            fwd_blocks<T, K, false>(col, ccr, y0, y1);
+#pragma unroll
+            for (int k = 0; k < MR; ++k) {
+                T f0, f1;
+                lds2(sm.cF[k][pw][ph2], f0, f1);
+                T gv = f0 * v[k];
+                if (K == 2) gv -= lds1(&sm.cF2[k][pw][ph2]) * y0;
+                gv -= f1 * y1;
+                y0 = y1;
+                y1 = gv;
+            }
             sm.cf[p][s][0] = y0;
             sm.cf[p][s][1] = y1;
-            const T *m = sm.sfx[p];
-            sm.red[p][s][0] = m[0] * y0 + m[1] * y1;
-            sm.red[p][s][1] = m[2] * y0 + m[3] * y1;
         }
         named_sync(1, NT);
+        // ---- exchange 1: this CTA's forward aggregate to every peer
         if (p == 0) {
             T a0 = T(0), a1 = T(0);
-#pragma unroll
-            for (int q = 0; q < PC; ++q) a0 += sm.red[q][s][0], a1 += sm.red[q][s][1];
+            for (int q = 0; q < PC; ++q) aff(a0, a1, sm.cf[q][s][0], sm.cf[q][s][1], sm.mf[q]);
             sm.agg[s][0] = a0;
             sm.agg[s][1] = a1;
         }
         named_sync(1, NT);
-        // ---- exchange 1: the aggregate to every peer (thread (p, s) -> peer p)
         if (p < C) {
             st_remote(&sm.aggF[c][s][0], (uint32_t)p, sm.agg[s][0]);
             st_remote(&sm.aggF[c][s][1], (uint32_t)p, sm.agg[s][1]);
         }
         named_sync(1, NT);
+        // one release-arrive per peer, issued by C threads in parallel (each
+        // release covers this CTA's DSMEM stores through the CTA barrier above)
+        if (tid < C) bar_arrive_remote(&sm.xf, (uint32_t)tid);
         if (tid == 0) {
-            for (int r = 0; r < C; ++r) bar_arrive_remote(&sm.xf, (uint32_t)r);
+            CLU_TR(2);
             bar_wait_cluster(&sm.xf, ph);   // one cluster-scope acquire, then a CTA barrier
+            CLU_TR(3);
         }
         named_sync(1, NT);
         // ---- sweep 2: forward with the true inflow: v <- g
         {
-            T f0 = T(0), f1 = T(0);   // CTA inflow
-            for (int cc = 0; cc < (int)c; ++cc) {
-                const T *m = sm.pcf[cc];
-                const T a0 = sm.aggF[cc][s][0], a1 = sm.aggF[cc][s][1];
-                f0 += m[0] * a0 + m[1] * a1;
-                f1 += m[2] * a0 + m[3] * a1;
+            T y0 = T(0), y1 = T(0);
+            for (int cc = 0; cc < (int)c; ++cc) aff(y0, y1, sm.aggF[cc][s][0], sm.aggF[cc][s][1], sm.mfc[cc]);
+            for (int q = 0; q < p; ++q) aff(y0, y1, sm.cf[q][s][0], sm.cf[q][s][1], sm.mf[q]);
+#pragma unroll
+            for (int k = 0; k < MR; ++k) {
+                T f0, f1;
+                lds2(sm.cF[k][pw][ph2], f0, f1);
+                T gv = f0 * v[k];
+                if (K == 2) gv -= lds1(&sm.cF2[k][pw][ph2]) * y0;
+                gv -= f1 * y1;
+                y0 = y1;
+                y1 = gv;
+                v[k] = gv;
             }
-            const T *ph_ = sm.phi[p];
-            T y0 = ph_[0] * f0 + ph_[1] * f1, y1 = ph_[2] * f0 + ph_[3] * f1;
-            {
-                T e0 = T(0), e1 = T(0);   // chunk-local exclusive prefix
-                for (int q = 0; q < p; ++q) aff(e0, e1, sm.cf[q][s][0], sm.cf[q][s][1], sm.mf[q]);
-                y0 += e0;
-                y1 += e1;
-            }
-            fwd_blocks<T, K, true>(col, ccr, y0, y1);
         }
-        named_sync(1, NT);   // cf, red are rewritten below
-        // ---- sweep 3: back substitution, zero inflow -> chunk carry and aggregate share
+        named_sync(1, NT);   // cf is rewritten below
+        // ---- sweep 3: back substitution, zero inflow -> chunk carry
         {
             T z0 = T(0), z1 = T(0);
-            bwd_blocks<T, K, false>(col, ccr, z0, z1);
+#pragma unroll
+            for (int k = MR - 1; k >= 0; --k) {
+                T b1, b2;
+                lds2(sm.cB[k][pw][ph2], b1, b2);
+                T xx = v[k];
+                if (K == 2) xx -= b2 * z1;
+                xx -= b1 * z0;
+                z1 = z0;
+                z0 = xx;
+            }
             sm.cf[p][s][0] = z0;
             sm.cf[p][s][1] = z1;
-            const T *m = sm.sbx[p];
-            sm.red[p][s][0] = m[0] * z0 + m[1] * z1;
-            sm.red[p][s][1] = m[2] * z0 + m[3] * z1;
         }
-        // (cyclic) forward values on the spec rows, g in v: owner thread -> every peer
+        // (cyclic) forward values on the spec rows (g in v): owner thread -> every peer
         if (PER) {
 #pragma unroll
             for (int jx = 0; jx < 4; ++jx) {
                 const int64_t sr = A.srow[jx] - row0 - k0;
                 if (A.srow[jx] >= 0 && sr >= 0 && sr < MR) {
-                    const T val = col[sr * W];
+                    T val = T(0);
+#pragma unroll
+                    for (int k = 0; k < MR; ++k)
+                        if (k == sr) val = v[k];
                     for (int r = 0; r < C; ++r) st_remote(&sm.spec[jx][s], (uint32_t)r, val);
                 }
             }
@@ -469,8 +479,7 @@ __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(cons
         named_sync(1, NT);
         if (p == 0) {
             T a0 = T(0), a1 = T(0);
-#pragma unroll
-            for (int q = 0; q < PC; ++q) a0 += sm.red[q][s][0], a1 += sm.red[q][s][1];
+            for (int q = PC - 1; q >= 0; --q) aff(a0, a1, sm.cf[q][s][0], sm.cf[q][s][1], sm.mb[q]);
             sm.agg[s][0] = a0;
             sm.agg[s][1] = a1;
         }
@@ -481,9 +490,13 @@ __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(cons
             st_remote(&sm.aggB[c][s][1], (uint32_t)p, sm.agg[s][1]);
         }
         named_sync(1, NT);
+        // one release-arrive per peer, issued by C threads in parallel (each
+        // release covers this CTA's DSMEM stores through the CTA barrier above)
+        if (tid < C) bar_arrive_remote(&sm.xb, (uint32_t)tid);
         if (tid == 0) {
-            for (int r = 0; r < C; ++r) bar_arrive_remote(&sm.xb, (uint32_t)r);
+            CLU_TR(4);
             bar_wait_cluster(&sm.xb, ph);
+            CLU_TR(5);
         }
         named_sync(1, NT);
         if (PER) {
@@ -505,45 +518,45 @@ __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(cons
                     xl0 = (y1 + T(sc[0]) * sm.spec[0][s]) / T(sc[1]);
                     xl1 = T(0);
                 }
-                sm.xl[s][0] = xl0;
-                sm.xl[s][1] = xl1;
+                sm.agg[s][0] = xl0;   // agg is free after exchange 2
+                sm.agg[s][1] = xl1;
             }
             named_sync(1, NT);
         }
         // ---- sweep 4: back substitution with the true inflow (+ cyclic correction), x -> buffer
         {
-            T b0 = T(0), b1 = T(0);   // CTA backward inflow
-            for (int cc = (int)c + 1; cc < C; ++cc) {
-                const T *m = sm.pcb[cc];
-                const T a0 = sm.aggB[cc][s][0], a1 = sm.aggB[cc][s][1];
-                b0 += m[0] * a0 + m[1] * a1;
-                b1 += m[2] * a0 + m[3] * a1;
+            T z0 = T(0), z1 = T(0);
+            for (int cc = C - 1; cc > (int)c; --cc) aff(z0, z1, sm.aggB[cc][s][0], sm.aggB[cc][s][1], sm.mbc[cc]);
+            for (int q = PC - 1; q > p; --q) aff(z0, z1, sm.cf[q][s][0], sm.cf[q][s][1], sm.mb[q]);
+#pragma unroll
+            for (int k = MR - 1; k >= 0; --k) {
+                T b1, b2;
+                lds2(sm.cB[k][pw][ph2], b1, b2);
+                T xx = v[k];
+                if (K == 2) xx -= b2 * z1;
+                xx -= b1 * z0;
+                z1 = z0;
+                z0 = xx;
+                v[k] = xx;
             }
-            const T *ps = sm.psi[p];
-            T z0 = ps[0] * b0 + ps[1] * b1, z1 = ps[2] * b0 + ps[3] * b1;
-            {
-                T e0 = T(0), e1 = T(0);
-                for (int q = PC - 1; q > p; --q) aff(e0, e1, sm.cf[q][s][0], sm.cf[q][s][1], sm.mb[q]);
-                z0 += e0;
-                z1 += e1;
-            }
-            bwd_blocks<T, K, true>(col, ccr, z0, z1);
             if (PER) {
                 // cyclic correction x - Z x_l (Navon eq:solve / Sherman–Morrison)
-                const T xl0 = sm.xl[s][0], xl1 = sm.xl[s][1];
+                const T xl0 = sm.agg[s][0], xl1 = sm.agg[s][1];
                 const int64_t rbase = row0 + k0;
-                const T *zz = A.coef + rbase * COEF_STRIDE + 6;   // Z1, Z2
-#pragma unroll 8
+                const T *zz = A.coef + rbase * COEF_STRIDE + 6;   // Z1, Z2 (L2, broadcast)
+#pragma unroll
                 for (int k = 0; k < MR; ++k) {
-                    T o = col[k * W] - __ldg(zz + k * COEF_STRIDE) * xl0;
+                    T o = v[k] - __ldg(zz + k * COEF_STRIDE) * xl0;
                     if (K == 2) {
                         o -= __ldg(zz + k * COEF_STRIDE + 1) * xl1;
                         if (rbase + k == A.n - 2) o = xl0;
                         if (rbase + k == A.n - 1) o = xl1;
                     }
-                    col[k * W] = o;
+                    v[k] = o;
                 }
             }
+#pragma unroll
+            for (int k = 0; k < MR; ++k) col[k * W] = v[k];
         }
         // ---- x out: one TMA store per 256-row box; the buffer is released one group later
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -554,10 +567,12 @@ __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(cons
             tma_store(&tmap, c0, (int)row0, c2, sm.buf[b]);
             tma_store(&tmap, c0, (int)row0 + 256, c2, sm.buf[b] + 256 * W);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            CLU_TR(6);
             if (pend >= 0) {
                 asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
                 bar_arrive(&sm.empty[pend]);
             }
+            CLU_TR(7);
         }
         pend = b;
     }

@@ -183,3 +183,13 @@ def test_deterministic_and_launch_counted():
     torch.cuda.synchronize()
     assert torch.equal(x1, x2)
     assert pb.launch_count() == 2
+
+
+@pytest.mark.parametrize("solver", ["tile", "cluster"])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_solvers_agree(solver, dtype, monkeypatch):
+    """The register-tile and the TMA cluster kernels (PB_SOLVER) both match the oracle."""
+    monkeypatch.setenv("PB_SOLVER", solver)
+    n, m = 3000, 48
+    got, ref, _ = run_penta(n, m, periodic=True, layout="interleaved", dtype=dtype, seed=77)
+    assert relerr(got, ref) <= TOL[dtype]

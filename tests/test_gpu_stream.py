@@ -93,13 +93,13 @@ def test_stream_solve_many_and_repeat():
 
 
 def test_stream_matches_cluster_path(monkeypatch):
-    """The streaming path and the cluster path (PB_NO_STREAM) agree to rounding."""
+    """The streaming path and the default (cluster) path agree to rounding."""
     n, m = 3000, 48
     a, b, c, d, e = synth.dd_penta(n, 1, seed=21)
     f = torch.from_numpy(synth.rhs_uniform(n, m, seed=22)).cuda()
     h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in (a, b, c, d, e)], batch=m, n=n, periodic=True)
     x1 = h.solve(f.clone())
-    monkeypatch.setenv("PB_NO_STREAM", "1")
+    monkeypatch.delenv("PB_STREAM")
     x2 = h.solve(f.clone())
     torch.cuda.synchronize()
     assert float((x1 - x2).abs().max() / x2.abs().max()) <= 1e-13
