@@ -287,8 +287,9 @@ def bench_penta(args, rank, world, dev):
         "value": value, "ms_per_step": ms / args.steps, "kern_ms": kern_ms_max, "launches": launches,
         "residual": res, "clocks": clk.summary(),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(f"band_tile_{args.dtype}"),
-                     "algorithmic_bytes_per_launch": alg_bytes, "kernel": "band_tile_kernel (pent_solve)",
+                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(f"pent_solve_{args.dtype}"),
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "kernel": "pent_solve = tp_pass_kernel<P1> + tp_scan_kernel + tp_pass_kernel<P2> (one call)",
                      "peak_source": peak_src},
         "e2e": {"value": round(e2e_val, 2), "unit": "Munknowns/s", "steps": e2e_steps,
                 "h2d_bytes_per_step": es * n * m, "d2h_bytes_per_step": es * n * m,

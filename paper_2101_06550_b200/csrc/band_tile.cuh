@@ -29,6 +29,18 @@ struct ClusterPlan {
     void *cc = nullptr;   // rows x 5 compact sweep coefficients (dtype)
 };
 
+// two-pass streaming solve plan (twopass.cuh): row records, chunk maps, cyclic-row responses (dtype)
+struct TwoPassPlan {
+    int ok = 0, nq = 0;
+    void *rec = nullptr, *ct = nullptr, *rsp = nullptr;
+    // per-handle carry scratch (cudaMalloc, grow-only).  Solves on different
+    // streams are ordered through `done`.  (Bulk-async copies out of
+    // cudaMallocAsync pool memory intermittently faulted or hung on B200.)
+    mutable void *scratch = nullptr;
+    mutable size_t scratch_bytes = 0;
+    mutable cudaEvent_t done = nullptr;
+};
+
 struct Band {
     int K = 2;  // 2 = penta, 1 = tri
     int64_t batch = 0, n = 0, lhs_count = 1;
@@ -41,6 +53,7 @@ struct Band {
     Plan plan;
     StreamPlan splan;
     ClusterPlan cplan;
+    TwoPassPlan tplan;
     int64_t srow[4] = {-1, -1, -1, -1};
     // per-system LHS
     void *pcoef = nullptr;    // dtype, [(i*8 + j) * batch + s]
@@ -67,6 +80,14 @@ struct Band {
         cudaFree(cplan.mfc);
         cudaFree(cplan.mbc);
         cudaFree(cplan.cc);
+        cudaFree(tplan.rec);
+        cudaFree(tplan.ct);
+        cudaFree(tplan.rsp);
+        if (tplan.done) {
+            cudaEventSynchronize(tplan.done);
+            cudaEventDestroy(tplan.done);
+        }
+        cudaFree(tplan.scratch);
     }
 };
 
@@ -234,6 +255,9 @@ int clu_max_clusters_f64(int C, int K, int periodic);
 int clu_max_clusters_f32(int C, int K, int periodic);
 constexpr int CLU_RC = 512;   // rows per CTA of the cluster solve
 int stream_max_ctas_f32(int K, int periodic);
+int twopass_build_tables(Band *h, cudaStream_t st);
+int launch_tp_f64(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st);
+int launch_tp_f32(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st);
 
 // per-(dtype, K) entry points, defined in banded_inst_*.cu
 int launch_tile_f64_k2(const Band *h, void *x, int layout, int64_t count, int64_t bstride, cudaStream_t st);

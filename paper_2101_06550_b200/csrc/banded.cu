@@ -716,6 +716,7 @@ static int factor_impl(Band *h, const double *a, const double *b, const double *
         }
         if ((rc = stream_build_tables(h, st))) return rc;
         if ((rc = cluster_build_tables(h, st))) return rc;
+        if ((rc = twopass_build_tables(h, st))) return rc;
     } else {
         const int64_t M = h->batch;
         double *pcD = nullptr;
@@ -773,15 +774,19 @@ static int solve_impl(const Band *h, void *rhs, int layout, int64_t count, int64
     if (rc) return rc;
     sx.out_to(rhs);
     const bool al = (uintptr_t)sx.dev % 16 == 0 && (h->batch * es) % 16 == 0 && (count == 1 || (bstride * es) % 16 == 0);
-    // interleaved shared-LHS solver: the TMA cluster kernel (default, fastest
-    // measured on B200 at the bench configuration), the
-    // register-tile cluster kernel (PB_SOLVER=tile) or the streaming two-phase
-    // kernel (PB_SOLVER=stream)
+    // interleaved shared-LHS solver: the two-pass TMA streaming solve (default,
+    // fastest measured on B200 at the bench configuration), the
+    // TMA cluster kernel (PB_SOLVER=cluster), the register-tile cluster kernel
+    // (PB_SOLVER=tile) or the persistent streaming kernel (PB_SOLVER=stream)
     const char *solver = getenv("PB_SOLVER");
     const bool want_stream = (solver && !strcmp(solver, "stream")) || getenv("PB_STREAM");
     const bool want_tile = solver && !strcmp(solver, "tile");
+    const bool want_clu = solver && !strcmp(solver, "cluster");
     const bool inter = h->shared() && layout == PB_INTERLEAVED && al;
-    if (inter && want_stream && h->splan.ok)
+    if (inter && !want_stream && !want_tile && !want_clu && h->tplan.ok)
+        rc = h->dtype == PB_F64 ? launch_tp_f64(h, sx.dev, count, bstride, st)
+                                : launch_tp_f32(h, sx.dev, count, bstride, st);
+    else if (inter && want_stream && h->splan.ok)
         rc = h->dtype == PB_F64 ? launch_stream_f64(h, sx.dev, count, bstride, st)
                                 : launch_stream_f32(h, sx.dev, count, bstride, st);
     else if (inter && !want_tile && h->cplan.ok)

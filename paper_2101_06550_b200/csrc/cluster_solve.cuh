@@ -33,7 +33,7 @@ namespace clu {
 constexpr int RC = 512;      // rows per CTA
 constexpr int MR = 32;       // rows per chunk
 constexpr int PC = RC / MR;  // chunks per CTA (16)
-constexpr int NB = 3;        // group buffers per CTA
+constexpr int NB = 2;        // group buffers per CTA
 constexpr int MAXC = 16;     // cluster size limit (non-portable above 8)
 
 template <typename T>
@@ -62,6 +62,15 @@ struct Smem {
     T spec[4][W];               // exchange 2: forward values on the cyclic rows (from their owner)
     T mf[PC][4], mb[PC][4];     // chunk transfer matrices
     T mfc[MAXC][4], mbc[MAXC][4];   // CTA block transfer matrices
+    alignas(16) T z[RC][2];               // cyclic correction vectors Z1, Z2 of this CTA's rows
+    // transfer-matrix products (prologue) turning every fold into independent
+    // 2x2 mat-vecs: TF[p][j] = Mf_{p-1} .. Mf_j (j <= p), TB[p][j] = Mb_p .. Mb_{j-1} (j >= p)
+    T TF[PC + 1][PC + 1][4];
+    T TB[PC + 1][PC + 1][4];
+    // CTA level, for this CTA c
+    T pcf[MAXC][4];             // Mfc_{c-1} .. Mfc_{c'+1}  (aggF of c' < c -> inflow of c)
+    T pcb[MAXC][4];             // Mbc_{c+1} .. Mbc_{c'-1}  (aggB of c' > c -> inflow of c)
+    T pcy[MAXC][4];             // Mbc_0 .. Mbc_{c'-1}      (aggB of c' -> x_0, x_1)
     uint64_t full[NB], empty[NB];
     uint64_t xf, xb;            // exchange barriers (C remote arrivals each)
 };
@@ -85,9 +94,13 @@ __device__ __forceinline__ unsigned long long clu_gtimer()
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
+#define CLU_TR2(k)                                                                       \
+    do {                                                                                 \
+        if (A.trace && t < 256) A.trace[((int64_t)blockIdx.x * 256 + t) * 16 + (k)] = clu_gtimer(); \
+    } while (0)
 #define CLU_TR(k)                                                                        \
     do {                                                                                 \
-        if (A.trace && tid == 0 && t < 256) A.trace[((int64_t)blockIdx.x * 256 + t) * 8 + (k)] = clu_gtimer(); \
+        if (A.trace && tid == 0 && t < 256) A.trace[((int64_t)blockIdx.x * 256 + t) * 16 + (k)] = clu_gtimer(); \
     } while (0)
 
 __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -135,6 +148,16 @@ __device__ __forceinline__ void bar_arrive_remote(uint64_t *b, uint32_t rank)
         "r"(rank)
         : "memory");
 }
+__device__ __forceinline__ void bar_arrive_remote_relaxed(uint64_t *b, uint32_t rank)
+{
+    asm volatile(
+        "{\n .reg .b32 ra;\n"
+        " mapa.shared::cluster.u32 ra, %0, %1;\n"
+        " mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [ra];\n}" ::"r"(su32(b)),
+        "r"(rank)
+        : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
 template <typename T>
 __device__ __forceinline__ void st_remote(T *p, uint32_t rank, T v);
 template <>
@@ -181,6 +204,14 @@ __device__ __forceinline__ void aff(T &y0, T &y1, T c0, T c1, const T *m)
     const T n1 = c1 + m[2] * y0 + m[3] * y1;
     y0 = n0;
     y1 = n1;
+}
+
+// a += m x (2x2 mat-vec accumulate)
+template <typename T>
+__device__ __forceinline__ void mva(T &a0, T &a1, const T *m, T x0, T x1)
+{
+    a0 += m[0] * x0 + m[1] * x1;
+    a1 += m[2] * x0 + m[3] * x1;
 }
 
 // read-only global load the compiler keeps in program order (bounds the
@@ -349,6 +380,46 @@ __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(cons
         sm.mfc[e / 4][e % 4] = A.mfc[e];
         sm.mbc[e / 4][e % 4] = A.mbc[e];
     }
+    for (int e = tid; e < RC * 2; e += blockDim.x) sm.z[e / 2][e % 2] = A.coef[(row0 + e / 2) * COEF_STRIDE + 6 + e % 2];
+    __syncthreads();
+    if (tid <= PC) {
+        const int pp = tid;
+        T m[4];
+        set_id(m);
+        for (int j = 0; j < 4; ++j) sm.TF[pp][pp][j] = m[j];
+        for (int j = pp - 1; j >= 0; --j) {
+            mm(m, sm.mf[j], m);
+            for (int e = 0; e < 4; ++e) sm.TF[pp][j][e] = m[e];
+        }
+    } else if (tid >= 32 && tid <= 32 + PC) {
+        const int pp = tid - 32;
+        T m[4];
+        set_id(m);
+        for (int j = 0; j < 4; ++j) sm.TB[pp][pp][j] = m[j];
+        for (int j = pp + 1; j <= PC; ++j) {
+            mm(m, sm.mb[j - 1], m);
+            for (int e = 0; e < 4; ++e) sm.TB[pp][j][e] = m[e];
+        }
+    } else if (tid == 64) {
+        T m[4];
+        set_id(m);
+        for (int cc = (int)c - 1; cc >= 0; --cc) {
+            for (int j = 0; j < 4; ++j) sm.pcf[cc][j] = m[j];
+            mm(m, sm.mfc[cc], m);
+        }
+        set_id(m);
+        for (int cc = (int)c + 1; cc < C; ++cc) {
+            for (int j = 0; j < 4; ++j) sm.pcb[cc][j] = m[j];
+            mm(m, sm.mbc[cc], m);
+        }
+    } else if (tid == 96) {
+        T m[4];
+        set_id(m);
+        for (int cc = 0; cc < C; ++cc) {
+            for (int j = 0; j < 4; ++j) sm.pcy[cc][j] = m[j];
+            mm(m, sm.mbc[cc], m);
+        }
+    }
     __syncthreads();
     if (C > 1) cg::this_cluster().sync();   // peers' barriers initialised before any remote arrive
 
@@ -382,12 +453,18 @@ __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(cons
         const int b = t % NB;
         const uint32_t ph = t & 1;
         CLU_TR(0);
+        if (tid == 0 && pend >= 0) {
+            // the previous group's TMA store has finished reading its buffer
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            bar_arrive(&sm.empty[pend]);
+        }
         bar_wait(&sm.full[b], (t / NB) & 1);
         CLU_TR(1);
         T *col = sm.buf[b] + s + k0 * W;   // row k of the chunk at col[k * W]
         T v[MR];
 #pragma unroll
         for (int k = 0; k < MR; ++k) v[k] = col[k * W];
+        CLU_TR(8);
 
         // ---- sweep 1: forward, zero inflow -> chunk carry
         {
@@ -405,24 +482,34 @@ __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(cons
             sm.cf[p][s][0] = y0;
             sm.cf[p][s][1] = y1;
         }
+        CLU_TR(9);
         named_sync(1, NT);
         // ---- exchange 1: this CTA's forward aggregate to every peer
         if (p == 0) {
             T a0 = T(0), a1 = T(0);
-            for (int q = 0; q < PC; ++q) aff(a0, a1, sm.cf[q][s][0], sm.cf[q][s][1], sm.mf[q]);
+            T e0 = T(0), e1 = T(0);
+#pragma unroll
+            for (int q = 0; q < PC; q += 2) {
+                mva(a0, a1, sm.TF[PC][q + 1], sm.cf[q][s][0], sm.cf[q][s][1]);
+                mva(e0, e1, sm.TF[PC][q + 2], sm.cf[q + 1][s][0], sm.cf[q + 1][s][1]);
+            }
+            a0 += e0;
+            a1 += e1;
             sm.agg[s][0] = a0;
             sm.agg[s][1] = a1;
         }
         named_sync(1, NT);
+        CLU_TR(10);
         if (p < C) {
             st_remote(&sm.aggF[c][s][0], (uint32_t)p, sm.agg[s][0]);
             st_remote(&sm.aggF[c][s][1], (uint32_t)p, sm.agg[s][1]);
         }
         named_sync(1, NT);
-        // one release-arrive per peer, issued by C threads in parallel (each
-        // release covers this CTA's DSMEM stores through the CTA barrier above)
-        if (tid < C) bar_arrive_remote(&sm.xf, (uint32_t)tid);
+        // one cluster-scope fence (covers this CTA's DSMEM stores through the
+        // CTA barrier above), then relaxed arrives on every peer's barrier
         if (tid == 0) {
+            fence_acq_rel_cluster();
+            for (int r = 0; r < C; ++r) bar_arrive_remote_relaxed(&sm.xf, (uint32_t)r);
             CLU_TR(2);
             bar_wait_cluster(&sm.xf, ph);   // one cluster-scope acquire, then a CTA barrier
             CLU_TR(3);
@@ -431,8 +518,21 @@ __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(cons
         // ---- sweep 2: forward with the true inflow: v <- g
         {
             T y0 = T(0), y1 = T(0);
-            for (int cc = 0; cc < (int)c; ++cc) aff(y0, y1, sm.aggF[cc][s][0], sm.aggF[cc][s][1], sm.mfc[cc]);
-            for (int q = 0; q < p; ++q) aff(y0, y1, sm.cf[q][s][0], sm.cf[q][s][1], sm.mf[q]);
+            {
+                T u0 = T(0), u1 = T(0);
+                for (int cc = 0; cc < (int)c; ++cc) mva(u0, u1, sm.pcf[cc], sm.aggF[cc][s][0], sm.aggF[cc][s][1]);
+                mva(y0, y1, sm.TF[p][0], u0, u1);
+                T e0 = T(0), e1 = T(0);
+#pragma unroll
+                for (int q = 0; q < PC - 1; ++q)
+                    if (q < p) {
+                        if (q & 1) mva(e0, e1, sm.TF[p][q + 1], sm.cf[q][s][0], sm.cf[q][s][1]);
+                        else mva(y0, y1, sm.TF[p][q + 1], sm.cf[q][s][0], sm.cf[q][s][1]);
+                    }
+                y0 += e0;
+                y1 += e1;
+            }
+            if (p == PC - 1 && s == 0) CLU_TR2(11);
 #pragma unroll
             for (int k = 0; k < MR; ++k) {
                 T f0, f1;
@@ -445,6 +545,7 @@ __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(cons
                 v[k] = gv;
             }
         }
+        if (p == PC - 1 && s == 0) CLU_TR2(12);
         named_sync(1, NT);   // cf is rewritten below
         // ---- sweep 3: back substitution, zero inflow -> chunk carry
         {
@@ -479,7 +580,14 @@ __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(cons
         named_sync(1, NT);
         if (p == 0) {
             T a0 = T(0), a1 = T(0);
-            for (int q = PC - 1; q >= 0; --q) aff(a0, a1, sm.cf[q][s][0], sm.cf[q][s][1], sm.mb[q]);
+            T e0 = T(0), e1 = T(0);
+#pragma unroll
+            for (int q = 0; q < PC; q += 2) {
+                mva(a0, a1, sm.TB[0][q], sm.cf[q][s][0], sm.cf[q][s][1]);
+                mva(e0, e1, sm.TB[0][q + 1], sm.cf[q + 1][s][0], sm.cf[q + 1][s][1]);
+            }
+            a0 += e0;
+            a1 += e1;
             sm.agg[s][0] = a0;
             sm.agg[s][1] = a1;
         }
@@ -490,10 +598,11 @@ __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(cons
             st_remote(&sm.aggB[c][s][1], (uint32_t)p, sm.agg[s][1]);
         }
         named_sync(1, NT);
-        // one release-arrive per peer, issued by C threads in parallel (each
-        // release covers this CTA's DSMEM stores through the CTA barrier above)
-        if (tid < C) bar_arrive_remote(&sm.xb, (uint32_t)tid);
+        // one cluster-scope fence (covers this CTA's DSMEM stores through the
+        // CTA barrier above), then relaxed arrives on every peer's barrier
         if (tid == 0) {
+            fence_acq_rel_cluster();
+            for (int r = 0; r < C; ++r) bar_arrive_remote_relaxed(&sm.xb, (uint32_t)r);
             CLU_TR(4);
             bar_wait_cluster(&sm.xb, ph);
             CLU_TR(5);
@@ -503,7 +612,7 @@ __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(cons
             // y = (x_0, x_1): the backward composition of every CTA; then the 2x2
             if (p == 0) {
                 T y1 = T(0), y2 = T(0);
-                for (int cc = C - 1; cc >= 0; --cc) aff(y1, y2, sm.aggB[cc][s][0], sm.aggB[cc][s][1], sm.mbc[cc]);
+                for (int cc = 0; cc < C; ++cc) mva(y1, y2, sm.pcy[cc], sm.aggB[cc][s][0], sm.aggB[cc][s][1]);
                 const double *sc = A.scal;
                 T xl0, xl1;
                 if (K == 2) {
@@ -526,8 +635,21 @@ __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(cons
         // ---- sweep 4: back substitution with the true inflow (+ cyclic correction), x -> buffer
         {
             T z0 = T(0), z1 = T(0);
-            for (int cc = C - 1; cc > (int)c; --cc) aff(z0, z1, sm.aggB[cc][s][0], sm.aggB[cc][s][1], sm.mbc[cc]);
-            for (int q = PC - 1; q > p; --q) aff(z0, z1, sm.cf[q][s][0], sm.cf[q][s][1], sm.mb[q]);
+            {
+                T u0 = T(0), u1 = T(0);
+                for (int cc = (int)c + 1; cc < C; ++cc) mva(u0, u1, sm.pcb[cc], sm.aggB[cc][s][0], sm.aggB[cc][s][1]);
+                mva(z0, z1, sm.TB[p + 1][PC], u0, u1);
+                T e0 = T(0), e1 = T(0);
+#pragma unroll
+                for (int q = 1; q < PC; ++q)
+                    if (q > p) {
+                        if (q & 1) mva(e0, e1, sm.TB[p + 1][q], sm.cf[q][s][0], sm.cf[q][s][1]);
+                        else mva(z0, z1, sm.TB[p + 1][q], sm.cf[q][s][0], sm.cf[q][s][1]);
+                    }
+                z0 += e0;
+                z1 += e1;
+            }
+            if (p == 0 && s == 0) CLU_TR(13);
 #pragma unroll
             for (int k = MR - 1; k >= 0; --k) {
                 T b1, b2;
@@ -539,22 +661,25 @@ __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(cons
                 z0 = xx;
                 v[k] = xx;
             }
+            if (p == 0 && s == 0) CLU_TR(14);
             if (PER) {
                 // cyclic correction x - Z x_l (Navon eq:solve / Sherman–Morrison)
                 const T xl0 = sm.agg[s][0], xl1 = sm.agg[s][1];
                 const int64_t rbase = row0 + k0;
-                const T *zz = A.coef + rbase * COEF_STRIDE + 6;   // Z1, Z2 (L2, broadcast)
 #pragma unroll
                 for (int k = 0; k < MR; ++k) {
-                    T o = v[k] - __ldg(zz + k * COEF_STRIDE) * xl0;
+                    T z1v, z2v;
+                    lds2(sm.z[k0 + k], z1v, z2v);
+                    T o = v[k] - z1v * xl0;
                     if (K == 2) {
-                        o -= __ldg(zz + k * COEF_STRIDE + 1) * xl1;
+                        o -= z2v * xl1;
                         if (rbase + k == A.n - 2) o = xl0;
                         if (rbase + k == A.n - 1) o = xl1;
                     }
                     v[k] = o;
                 }
             }
+            if (p == 0 && s == 0) CLU_TR(15);
 #pragma unroll
             for (int k = 0; k < MR; ++k) col[k * W] = v[k];
         }
@@ -568,10 +693,6 @@ __global__ void __launch_bounds__(Geom<T>::NT + 32, 1) cluster_solve_kernel(cons
             tma_store(&tmap, c0, (int)row0 + 256, c2, sm.buf[b] + 256 * W);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             CLU_TR(6);
-            if (pend >= 0) {
-                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-                bar_arrive(&sm.empty[pend]);
-            }
             CLU_TR(7);
         }
         pend = b;

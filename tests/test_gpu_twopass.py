@@ -1,0 +1,113 @@
+"""GPU parity of the two-pass streaming solve (twopass.cuh): the interleaved
+shared-LHS path of pent_solve / tri_solve with 64-row chunks, at sizes spanning
+one to hundreds of chunks, ragged last chunks (down to one row), system counts
+that are not multiples of the warp or CTA width, several L2 slabs, cyclic and
+non-cyclic, fp64 (<= 1e-12) and fp32 (<= 1e-5 against the fp64 oracle)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2101_06550_b200 as pb  # noqa: E402
+
+
+@pytest.fixture(autouse=True)
+def _tp_path(monkeypatch):
+    monkeypatch.delenv("PB_SOLVER", raising=False)
+
+
+TOL = {"f64": 1e-12, "f32": 1e-5}
+TDT = {"f64": torch.float64, "f32": torch.float32}
+
+
+def relerr(x, ref):
+    return float(np.max(np.abs(x - ref)) / max(np.max(np.abs(ref)), 1e-300))
+
+
+# (n, m): n = 4 .. 16384 rows (1 .. 256 chunks, last chunk 1..64 rows), m odd / tiny / > one CTA
+SIZES = [(8, 4), (9, 4), (64, 16), (65, 36), (129, 132), (200, 8), (1000, 64), (2049, 40), (5000, 260), (16384, 4)]
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("periodic", [False, True])
+@pytest.mark.parametrize("n,m", SIZES)
+def test_tp_penta(n, m, periodic, dtype):
+    a, b, c, d, e = synth.dd_penta(n, 1, seed=n)
+    f = synth.rhs_uniform(n, m, seed=m + 1)
+    ref = oracle.penta_batch_solve(a, b, c, d, e, f, n=n, m=m, periodic=periodic)
+    h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in (a, b, c, d, e)], batch=m, n=n, periodic=periodic,
+                       dtype=dtype)
+    x = torch.from_numpy(f).to(TDT[dtype]).cuda()
+    h.solve(x)
+    torch.cuda.synchronize()
+    assert relerr(x.double().cpu().numpy(), ref) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("periodic", [False, True])
+@pytest.mark.parametrize("n,m", SIZES)
+def test_tp_tri(n, m, periodic, dtype):
+    a, b, c = synth.dd_tri(n, 1, seed=n + 3)
+    f = synth.rhs_uniform(n, m, seed=m + 2)
+    ref = oracle.tri_batch_solve(a, b, c, f, n=n, m=m, periodic=periodic)
+    h = pb.tri_factor(*[torch.from_numpy(v).cuda() for v in (a, b, c)], batch=m, n=n, periodic=periodic, dtype=dtype)
+    x = torch.from_numpy(f).to(TDT[dtype]).cuda()
+    h.solve(x)
+    torch.cuda.synchronize()
+    assert relerr(x.double().cpu().numpy(), ref) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("n", [300, 2048, 8192])
+def test_tp_thesis_matrix(n, dtype):
+    """The thesis CH operator (sigma = 45.09, kappa = 722), cyclic: the bench matrix."""
+    m = 64
+    s_ = synth.SIGMA_STATS
+    diags = synth.const_penta(n, s_, -4 * s_, 1 + 6 * s_, -4 * s_, s_)
+    f = synth.rhs_uniform(n, m, seed=n)
+    ref = oracle.penta_batch_solve(*diags, f, n=n, m=m, periodic=True)
+    h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in diags], batch=m, n=n, periodic=True, dtype=dtype)
+    x = torch.from_numpy(f).to(TDT[dtype]).cuda()
+    h.solve(x)
+    torch.cuda.synchronize()
+    assert relerr(x.double().cpu().numpy(), ref) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("slab_mb", ["0", "0.05", "1"])
+def test_tp_slabs_and_many(monkeypatch, slab_mb):
+    """count > 1 batches at a batch stride larger than batch*n, the systems split
+    into L2 slabs (PB_TP_SLAB_MB), repeated launches."""
+    monkeypatch.setenv("PB_TP_SLAB_MB", slab_mb)
+    n, m, cnt, pad = 1100, 300, 3, 17
+    a, b, c, d, e = synth.dd_penta(n, 1, seed=11)
+    f = synth.rhs_uniform(n, cnt * m, seed=12)
+    ref = np.concatenate([oracle.penta_batch_solve(a, b, c, d, e, f[k * n * m:(k + 1) * n * m], n=n, m=m,
+                                                   periodic=True) for k in range(cnt)])
+    h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in (a, b, c, d, e)], batch=m, n=n, periodic=True)
+    bs = n * m + pad
+    for _ in range(2):
+        buf = torch.full((cnt * bs,), 7.0, dtype=torch.float64, device="cuda")
+        for k in range(cnt):
+            buf[k * bs:k * bs + n * m] = torch.from_numpy(f[k * n * m:(k + 1) * n * m]).cuda()
+        h.solve_many(buf, cnt, bs)
+        torch.cuda.synchronize()
+        got = np.concatenate([buf[k * bs:k * bs + n * m].cpu().numpy() for k in range(cnt)])
+        assert relerr(got, ref) <= 1e-12
+        assert bool((buf.view(cnt, bs)[:, n * m:] == 7.0).all())   # padding untouched
+
+
+def test_tp_matches_cluster_path(monkeypatch):
+    """The two-pass path and the TMA cluster path agree to rounding."""
+    n, m = 3000, 48
+    a, b, c, d, e = synth.dd_penta(n, 1, seed=21)
+    f = torch.from_numpy(synth.rhs_uniform(n, m, seed=22)).cuda()
+    h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in (a, b, c, d, e)], batch=m, n=n, periodic=True)
+    x1 = h.solve(f.clone())
+    monkeypatch.setenv("PB_SOLVER", "cluster")
+    x2 = h.solve(f.clone())
+    torch.cuda.synchronize()
+    assert float((x1 - x2).abs().max() / x2.abs().max()) <= 1e-13

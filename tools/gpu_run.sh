@@ -6,6 +6,6 @@ timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 --adi-steps 5 --no-cpu > gpurun_out/ncu_launch.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:band_tile -s 4 -c 1 -o gpurun_out/prof_band python bench.py --steps 3 --warmup 3 --no-cpu --no-adi > gpurun_out/ncu_full1.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:adi_pass -s 6 -c 2 -o gpurun_out/prof_adi python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/ncu_full2.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:tp_ -s 7 -c 3 -o gpurun_out/prof_band python bench.py --steps 3 --warmup 3 --no-cpu --no-adi --no-dist > gpurun_out/ncu_full1.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:adi_pass -s 6 -c 2 -o gpurun_out/prof_adi python bench.py --steps 3 --warmup 3 --no-cpu --no-dist > gpurun_out/ncu_full2.log 2>&1
 ls -la gpurun_out

@@ -31,8 +31,8 @@ with open(os.path.join(out, f"{tag}_ncu_full.jsonl"), "w") as f:
 traffic = {}
 for r in rows:
     t = r.get("dram_read", 0) + r.get("dram_write", 0)
-    if "band_tile" in r["kernel"]:
-        traffic["band_tile_f64"] = t
+    if "tp_" in r["kernel"]:   # pass 1 + scan + pass 2 of one pent_solve
+        traffic["pent_solve_f64"] = traffic.get("pent_solve_f64", 0) + t
     if "adi_pass" in r["kernel"]:
         traffic["adi_step_f64"] = traffic.get("adi_step_f64", 0) + t
 json.dump(traffic, open(os.path.join(out, "ncu_traffic.json"), "w"), indent=1)
