@@ -419,10 +419,10 @@ __device__ __forceinline__ void ldm4(const T *p, T *m)
 // writing the inflows.  Records move in register batches of SB chunks.
 constexpr int NSEG = 8, SB = 8;
 
-template <typename T>
+template <typename T, int NW = NSEG>
 struct ScanSmem {
-    T agg[NSEG][TW][2];
-    T pm[NSEG][4];
+    T agg[NW][TW][2];
+    T pm[NW][4];
     T gsp[4][TW];
 };
 
@@ -584,6 +584,139 @@ __global__ void __launch_bounds__(32 * NSEG) tp_scan_kernel(const Args<T> A)
     if (PER && w == 0 && sys % A.msp < A.ms) {
         // (x_0, x_1) of the non-cyclic solution = warp 0's z after its walk
         const T y1c = z0, y2c = z1;
+        T g[4];
+#pragma unroll
+        for (int jx = 0; jx < 4; ++jx) g[jx] = A.srow[jx] >= 0 ? S.gsp[jx][lane] : T(0);
+        const double *sc = A.scal;
+        T xl0, xl1;
+        if (K == 2) {
+            // Navon (eq:first_two)
+            const T ym1 = g[1], ym2 = g[0] - T(sc[10]) * g[1];
+            const T q0 = g[2] - (T(sc[4]) * y1c + T(sc[5]) * ym2 + T(sc[6]) * ym1);
+            const T q1 = g[3] - (T(sc[7]) * y1c + T(sc[8]) * y2c + T(sc[9]) * ym1);
+            xl0 = T(sc[0]) * q0 + T(sc[1]) * q1;
+            xl1 = T(sc[2]) * q0 + T(sc[3]) * q1;
+        } else {
+            // Sherman–Morrison
+            xl0 = (y1c + T(sc[0]) * g[0]) / T(sc[1]);
+            xl1 = T(0);
+        }
+        A.xl[sys * 2 + 0] = xl0;
+        A.xl[sys * 2 + 1] = xl1;
+    }
+}
+
+// Register-resident scan (nq <= NW * CPS): the same segment scheme with NW = 16
+// warps and each warp's <= CPS chunk records held in registers between the
+// folds and walks, so the records are loaded once and stored once.
+constexpr int NSEG_R = 16, CPS_R = 8;
+
+template <typename T, int K, bool PER>
+__global__ void __launch_bounds__(32 * NSEG_R) tp_scan_reg_kernel(const Args<T> A)
+{
+    constexpr int NW = NSEG_R, CPS = CPS_R;
+    __shared__ ScanSmem<T, NW> S;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t nsys = A.msp * A.count;
+    const int64_t sys = (int64_t)blockIdx.x * TW + lane;
+    const int nq = A.nq, cps = (nq + NW - 1) / NW;
+    const int qa = min(nq, w * cps), cnt = min(nq, qa + cps) - qa;
+    T *car = A.car + sys * 4;
+    const int64_t qstride = nsys * 4;
+    T R[CPS][4];
+#pragma unroll
+    for (int i = 0; i < CPS; ++i)
+        if (i < cnt) ld_rec(car + (qa + i) * qstride, R[i]);
+    // ---- forward fold of my segment
+    T P[4] = {T(1), T(0), T(0), T(1)}, a0 = T(0), a1 = T(0);
+#pragma unroll
+    for (int i = 0; i < CPS; ++i)
+        if (i < cnt) {
+            T m[4], t0, t1;
+            ldm4(A.ct + (int64_t)(qa + i) * 12, m);
+            mv(m, a0, a1, t0, t1);
+            a0 = t0 + R[i][0];
+            a1 = t1 + R[i][1];
+            mmul(m, P, P);
+        }
+    S.agg[w][lane][0] = a0;
+    S.agg[w][lane][1] = a1;
+    if (lane == 0)
+        for (int e = 0; e < 4; ++e) S.pm[w][e] = P[e];
+    __syncthreads();
+    T y0 = T(0), y1 = T(0);
+    for (int v = 0; v < w; ++v) {
+        T t0, t1;
+        mv(S.pm[v], y0, y1, t0, t1);
+        y0 = t0 + S.agg[v][lane][0];
+        y1 = t1 + S.agg[v][lane][1];
+    }
+    // ---- forward walk: yin_q, c_q = zB_q + H_q yin_q; cyclic rows' true g
+#pragma unroll
+    for (int i = 0; i < CPS; ++i)
+        if (i < cnt) {
+            const int q = qa + i;
+            T m[4], h[4], t0, t1;
+            ldm4(A.ct + (int64_t)q * 12, m);
+            ldm4(A.ct + (int64_t)q * 12 + 8, h);
+            const T yf0 = R[i][0], yf1 = R[i][1];
+            mv(h, y0, y1, t0, t1);
+            R[i][0] = y0;
+            R[i][1] = y1;
+            R[i][2] += t0;
+            R[i][3] += t1;
+            if (PER && q >= A.qspec) {
+#pragma unroll
+                for (int jx = 0; jx < 4; ++jx)
+                    if (A.srow[jx] >= 0 && A.srow[jx] / Q == q)
+                        S.gsp[jx][lane] = A.spec[sys * 4 + jx] + A.rsp[jx * 2] * y0 + A.rsp[jx * 2 + 1] * y1;
+            }
+            mv(m, y0, y1, t0, t1);
+            y0 = t0 + yf0;
+            y1 = t1 + yf1;
+        }
+    // ---- backward fold of my segment (high to low)
+    T Pb[4] = {T(1), T(0), T(0), T(1)}, c0 = T(0), c1 = T(0);
+#pragma unroll
+    for (int i = CPS - 1; i >= 0; --i)
+        if (i < cnt) {
+            T m[4], t0, t1;
+            ldm4(A.ct + (int64_t)(qa + i) * 12 + 4, m);
+            mv(m, c0, c1, t0, t1);
+            c0 = t0 + R[i][2];
+            c1 = t1 + R[i][3];
+            mmul(m, Pb, Pb);
+        }
+    __syncthreads();   // forward aggregates consumed
+    S.agg[w][lane][0] = c0;
+    S.agg[w][lane][1] = c1;
+    if (lane == 0)
+        for (int e = 0; e < 4; ++e) S.pm[w][e] = Pb[e];
+    __syncthreads();
+    T z0 = T(0), z1 = T(0);
+    for (int v = NW - 1; v > w; --v) {
+        T t0, t1;
+        mv(S.pm[v], z0, z1, t0, t1);
+        z0 = t0 + S.agg[v][lane][0];
+        z1 = t1 + S.agg[v][lane][1];
+    }
+#pragma unroll
+    for (int i = CPS - 1; i >= 0; --i)
+        if (i < cnt) {
+            T m[4], t0, t1;
+            ldm4(A.ct + (int64_t)(qa + i) * 12 + 4, m);
+            const T cq0 = R[i][2], cq1 = R[i][3];
+            R[i][2] = z0;
+            R[i][3] = z1;
+            mv(m, z0, z1, t0, t1);
+            z0 = t0 + cq0;
+            z1 = t1 + cq1;
+        }
+#pragma unroll
+    for (int i = 0; i < CPS; ++i)
+        if (i < cnt) st_rec(car + (qa + i) * qstride, R[i]);
+    if (PER && w == 0 && sys % A.msp < A.ms) {
+        const T y1c = z0, y2c = z1;   // (x_0, x_1) of the non-cyclic solution
         T g[4];
 #pragma unroll
         for (int jx = 0; jx < 4; ++jx) g[jx] = A.srow[jx] >= 0 ? S.gsp[jx][lane] : T(0);
