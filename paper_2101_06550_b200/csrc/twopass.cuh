@@ -45,7 +45,13 @@ namespace tp {
 constexpr int Q = 64;       // rows per chunk (tile height)
 constexpr int TW = 32;      // systems per tile (lanes)
 constexpr int REC = 6;      // pass-1 row record length
-constexpr int NWC = 4;      // consumer warps per CTA
+constexpr int NWC = 4;      // consumer warps per CTA, pass 2
+#ifndef TP_NWC1
+#define TP_NWC1 4
+#endif
+constexpr int NWC1 = TP_NWC1;   // consumer warps per CTA, pass 1
+template <bool P2>
+__host__ __device__ constexpr int nwc() { return P2 ? NWC : NWC1; }
 
 template <typename T>
 struct Cfg {
@@ -258,7 +264,7 @@ __device__ __forceinline__ void load_inflow(const Args<T> &A, int64_t t, int lan
 }
 
 template <typename T, int K, bool PER, bool P2>
-__global__ void __launch_bounds__(32 * (NWC + 1), 1) tp_pass_kernel(const __grid_constant__ CUtensorMap tmap,
+__global__ void __launch_bounds__(32 * (nwc<P2>() + 1), 1) tp_pass_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                      const __grid_constant__ CUtensorMap smap,
                                                                      const Args<T> A)
 {
@@ -278,7 +284,8 @@ __global__ void __launch_bounds__(32 * (NWC + 1), 1) tp_pass_kernel(const __grid
     }
     __syncthreads();
 
-    if (warp == NWC) {
+    constexpr int NC = nwc<P2>();
+    if (warp == NC) {
         // ---------------- producer
         if (lane != 0) return;
         // L2 hint only for pass 1 of a slabbed solve (keep the slab for pass 2).
@@ -318,9 +325,9 @@ __global__ void __launch_bounds__(32 * (NWC + 1), 1) tp_pass_kernel(const __grid
     int j = warp;
     bool pend = false;
     T pf[6];   // pass 2: the next tile's (yin, zin, x_l) of this lane, loaded one tile ahead
-    const int64_t tstep = (int64_t)NWC * gridDim.x;
+    const int64_t tstep = (int64_t)NC * gridDim.x;
     if (P2 && blockIdx.x + (int64_t)warp * gridDim.x < ntile) load_inflow<T, PER>(A, blockIdx.x + (int64_t)warp * gridDim.x, lane, pf);
-    for (int64_t t = blockIdx.x + (int64_t)warp * gridDim.x; t < ntile; t += tstep, j += NWC) {
+    for (int64_t t = blockIdx.x + (int64_t)warp * gridDim.x; t < ntile; t += tstep, j += NC) {
         const int sl = j % NS;
         bar_wait(&sm.full[sl], (j / NS) & 1);
         const TileId id = tile_of(t, A.G, A.count);
