@@ -25,6 +25,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 
 #include "band_tile.cuh"
 
@@ -298,6 +299,31 @@ static int adi_band(int64_t n, double sigma, int dtype, cudaStream_t st, Band **
     return PB_OK;
 }
 
+// C^{n+1} = Cbar^{n+1} + v = 2 C^n - C^{n-1} + v, written over C^{n-1} (16-byte vectors)
+template <typename T>
+__global__ void adi_combine_kernel(int64_t count, const T *__restrict__ cn, T *__restrict__ cm, const T *__restrict__ v)
+{
+    using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+    constexpr int E = 16 / sizeof(T);
+    const int64_t nv = count / E;
+    const V *a = reinterpret_cast<const V *>(cn);
+    const V *c = reinterpret_cast<const V *>(v);
+    V *b = reinterpret_cast<V *>(cm);
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nv; k += (int64_t)gridDim.x * blockDim.x) {
+        const V x = __ldcs(a + k), y = __ldcs(b + k), z = __ldcs(c + k);
+        V o;
+        const T *xs = reinterpret_cast<const T *>(&x), *ys = reinterpret_cast<const T *>(&y),
+                *zs = reinterpret_cast<const T *>(&z);
+        T *os = reinterpret_cast<T *>(&o);
+#pragma unroll
+        for (int e = 0; e < E; ++e) os[e] = (T(2) * xs[e] - ys[e]) + zs[e];
+        __stcs(b + k, o);
+    }
+    for (int64_t k = nv * E + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count;
+         k += (int64_t)gridDim.x * blockDim.x)
+        cm[k] = (T(2) * cn[k] - cm[k]) + v[k];
+}
+
 template <typename T>
 static int adi_run(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nsteps, cudaStream_t st)
 {
@@ -321,11 +347,28 @@ static int adi_run(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nst
     A.k_bih = T(-(2.0 / 3.0) * dt * p->D * p->gamma / (dx * dx * dx * dx));
     A.k_lap = T((2.0 / 3.0) * p->D * dt / (dx * dx));
     A.w = (T *)s->work;
+    // y-sweep path: the two-pass solve (default) or the fused band_core pass B (PB_ADI_YSWEEP=band)
+    const char *ys = getenv("PB_ADI_YSWEEP");
+    const bool ysweep_tp = h->tplan.ok && !(ys && !strcmp(ys, "band")) && (n * (int64_t)sizeof(T)) % 16 == 0 &&
+                           (uintptr_t)s->work % 16 == 0 && (uintptr_t)s->c_cur % 16 == 0 &&
+                           (uintptr_t)s->c_prev % 16 == 0;
     for (int64_t step = 0; step < nsteps; ++step) {
         A.cn = (const T *)s->c_cur;
         A.cm = (T *)s->c_prev;
         if ((rc = launch_adi_cfg<T>(h, A, s->sims, st, true))) return rc;
-        if ((rc = launch_adi_cfg<T>(h, A, s->sims, st, false))) return rc;
+        if (ysweep_tp) {
+            // y-sweep = the batched interleaved solve (systems = columns i, one batch
+            // per simulation) by the two-pass TMA solve, then the C^{n+1} combine
+            rc = sizeof(T) == 8 ? launch_tp_f64(h, A.w, s->sims, n * n, st) : launch_tp_f32(h, A.w, s->sims, n * n, st);
+            if (rc) return rc;
+            int dev = 0, nsm = 0;
+            PB_CUDA_TRY(cudaGetDevice(&dev));
+            PB_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+            adi_combine_kernel<T><<<(unsigned)(nsm * 8), 256, 0, st>>>(s->sims * n * n, A.cn, A.cm, A.w);
+            PB_LAUNCH_CHECK();
+        } else if ((rc = launch_adi_cfg<T>(h, A, s->sims, st, false))) {
+            return rc;
+        }
         void *t = s->c_prev;  // C^{n+1} now lives in the old C^{n-1} buffer
         s->c_prev = s->c_cur;
         s->c_cur = t;
