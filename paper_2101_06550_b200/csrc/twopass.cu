@@ -202,7 +202,7 @@ static int launch_tp_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
         A.G = (int)((A.ms + tp::TW - 1) / tp::TW);
         const int64_t ntile = (int64_t)nq * A.G * count;
         const unsigned grid = (unsigned)(ntile < nsm ? ntile : nsm);
-        tp::tp_pass_kernel<T, K, PER, false><<<grid, 32 * (tp::NWC + 1), sm1, st>>>(tmap, smap, A);
+        tp::tp_pass_kernel<T, K, PER, false><<<grid, 32 * (tp::NWC1 + 1), sm1, st>>>(tmap, smap, A);
         PB_LAUNCH_CHECK();
         if (nq <= tp::NSEG_R * tp::CPS_R)
             tp::tp_scan_reg_kernel<T, K, PER><<<(unsigned)(nsys / tp::TW), 32 * tp::NSEG_R, 0, st>>>(A);
