@@ -618,11 +618,19 @@ __global__ void __launch_bounds__(32 * NSEG) tp_scan_kernel(const Args<T> A)
 // folds and walks, so the records are loaded once and stored once.
 constexpr int NSEG_R = 16, CPS_R = 8;
 
+template <typename T>
+__device__ __forceinline__ void ldm4s(const T *p, T *m)
+{
+    lds2(p, m[0], m[1]);
+    lds2(p + 2, m[2], m[3]);
+}
+
 template <typename T, int K, bool PER>
 __global__ void __launch_bounds__(32 * NSEG_R) tp_scan_reg_kernel(const Args<T> A)
 {
     constexpr int NW = NSEG_R, CPS = CPS_R;
     __shared__ ScanSmem<T, NW> S;
+    __shared__ __align__(16) T cts[NW * CPS][12];   // the chunk maps, staged once per CTA
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t nsys = A.msp * A.count;
     const int64_t sys = (int64_t)blockIdx.x * TW + lane;
@@ -630,17 +638,19 @@ __global__ void __launch_bounds__(32 * NSEG_R) tp_scan_reg_kernel(const Args<T> 
     const int qa = min(nq, w * cps), cnt = min(nq, qa + cps) - qa;
     T *car = A.car + sys * 4;
     const int64_t qstride = nsys * 4;
+    for (int e = threadIdx.x; e < nq * 12; e += blockDim.x) (&cts[0][0])[e] = A.ct[e];
     T R[CPS][4];
 #pragma unroll
     for (int i = 0; i < CPS; ++i)
         if (i < cnt) ld_rec(car + (qa + i) * qstride, R[i]);
+    __syncthreads();   // chunk maps staged
     // ---- forward fold of my segment
     T P[4] = {T(1), T(0), T(0), T(1)}, a0 = T(0), a1 = T(0);
 #pragma unroll
     for (int i = 0; i < CPS; ++i)
         if (i < cnt) {
             T m[4], t0, t1;
-            ldm4(A.ct + (int64_t)(qa + i) * 12, m);
+            ldm4s(cts[qa + i], m);
             mv(m, a0, a1, t0, t1);
             a0 = t0 + R[i][0];
             a1 = t1 + R[i][1];
@@ -664,8 +674,8 @@ __global__ void __launch_bounds__(32 * NSEG_R) tp_scan_reg_kernel(const Args<T> 
         if (i < cnt) {
             const int q = qa + i;
             T m[4], h[4], t0, t1;
-            ldm4(A.ct + (int64_t)q * 12, m);
-            ldm4(A.ct + (int64_t)q * 12 + 8, h);
+            ldm4s(cts[q], m);
+            ldm4s(cts[q] + 8, h);
             const T yf0 = R[i][0], yf1 = R[i][1];
             mv(h, y0, y1, t0, t1);
             R[i][0] = y0;
@@ -688,7 +698,7 @@ __global__ void __launch_bounds__(32 * NSEG_R) tp_scan_reg_kernel(const Args<T> 
     for (int i = CPS - 1; i >= 0; --i)
         if (i < cnt) {
             T m[4], t0, t1;
-            ldm4(A.ct + (int64_t)(qa + i) * 12 + 4, m);
+            ldm4s(cts[qa + i] + 4, m);
             mv(m, c0, c1, t0, t1);
             c0 = t0 + R[i][2];
             c1 = t1 + R[i][3];
@@ -711,7 +721,7 @@ __global__ void __launch_bounds__(32 * NSEG_R) tp_scan_reg_kernel(const Args<T> 
     for (int i = CPS - 1; i >= 0; --i)
         if (i < cnt) {
             T m[4], t0, t1;
-            ldm4(A.ct + (int64_t)(qa + i) * 12 + 4, m);
+            ldm4s(cts[qa + i] + 4, m);
             const T cq0 = R[i][2], cq1 = R[i][3];
             R[i][2] = z0;
             R[i][3] = z1;
