@@ -204,7 +204,9 @@ static int launch_tp_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
         const unsigned grid = (unsigned)(ntile < nsm ? ntile : nsm);
         tp::tp_pass_kernel<T, K, PER, false><<<grid, 32 * (tp::NWC1 + 1), sm1, st>>>(tmap, smap, A);
         PB_LAUNCH_CHECK();
-        if (nq <= tp::NSEG_R * tp::CPS_R)
+        if (nq <= tp::SEQ_MAX)
+            tp::tp_scan_seq_kernel<T, K, PER><<<(unsigned)((nsys + 255) / 256), 256, 0, st>>>(A);
+        else if (nq <= tp::NSEG_R * tp::CPS_R)
             tp::tp_scan_reg_kernel<T, K, PER><<<(unsigned)(nsys / tp::TW), 32 * tp::NSEG_R, 0, st>>>(A);
         else
             tp::tp_scan_kernel<T, K, PER><<<(unsigned)(nsys / tp::TW), 32 * tp::NSEG, 0, st>>>(A);

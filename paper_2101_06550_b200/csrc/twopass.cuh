@@ -756,5 +756,86 @@ __global__ void __launch_bounds__(32 * NSEG_R) tp_scan_reg_kernel(const Args<T> 
     }
 }
 
+// Short systems (nq <= SEQ_MAX chunks): one thread per system walks its chunks
+// sequentially with the records in registers (no cross-warp combine); the
+// chunk maps are staged in shared memory per CTA.
+constexpr int SEQ_MAX = 16;
+
+template <typename T, int K, bool PER>
+__global__ void __launch_bounds__(256) tp_scan_seq_kernel(const Args<T> A)
+{
+    __shared__ __align__(16) T cts[SEQ_MAX][12];
+    const int nq = A.nq;
+    for (int e = threadIdx.x; e < nq * 12; e += blockDim.x) (&cts[0][0])[e] = A.ct[e];
+    __syncthreads();
+    const int64_t nsys = A.msp * A.count;
+    const int64_t sys = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (sys >= nsys) return;
+    T *car = A.car + sys * 4;
+    const int64_t qstride = nsys * 4;
+    T R[SEQ_MAX][4];
+#pragma unroll
+    for (int q = 0; q < SEQ_MAX; ++q)
+        if (q < nq) ld_rec(car + q * qstride, R[q]);
+    T y0 = T(0), y1 = T(0), g[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+    for (int q = 0; q < SEQ_MAX; ++q)
+        if (q < nq) {
+            T m[4], h[4], t0, t1;
+            ldm4s(cts[q], m);
+            ldm4s(cts[q] + 8, h);
+            const T yf0 = R[q][0], yf1 = R[q][1];
+            mv(h, y0, y1, t0, t1);
+            R[q][0] = y0;
+            R[q][1] = y1;
+            R[q][2] += t0;
+            R[q][3] += t1;
+            if (PER && q >= A.qspec) {
+#pragma unroll
+                for (int jx = 0; jx < 4; ++jx)
+                    if (A.srow[jx] >= 0 && A.srow[jx] / Q == q)
+                        g[jx] = A.spec[sys * 4 + jx] + A.rsp[jx * 2] * y0 + A.rsp[jx * 2 + 1] * y1;
+            }
+            mv(m, y0, y1, t0, t1);
+            y0 = t0 + yf0;
+            y1 = t1 + yf1;
+        }
+    T z0 = T(0), z1 = T(0);
+#pragma unroll
+    for (int q = SEQ_MAX - 1; q >= 0; --q)
+        if (q < nq) {
+            T m[4], t0, t1;
+            ldm4s(cts[q] + 4, m);
+            const T cq0 = R[q][2], cq1 = R[q][3];
+            R[q][2] = z0;
+            R[q][3] = z1;
+            mv(m, z0, z1, t0, t1);
+            z0 = t0 + cq0;
+            z1 = t1 + cq1;
+        }
+#pragma unroll
+    for (int q = 0; q < SEQ_MAX; ++q)
+        if (q < nq) st_rec(car + q * qstride, R[q]);
+    if (PER && sys % A.msp < A.ms) {
+        const T y1c = z0, y2c = z1;   // (x_0, x_1) of the non-cyclic solution
+        const double *sc = A.scal;
+        T xl0, xl1;
+        if (K == 2) {
+            // Navon (eq:first_two)
+            const T ym1 = g[1], ym2 = g[0] - T(sc[10]) * g[1];
+            const T q0 = g[2] - (T(sc[4]) * y1c + T(sc[5]) * ym2 + T(sc[6]) * ym1);
+            const T q1 = g[3] - (T(sc[7]) * y1c + T(sc[8]) * y2c + T(sc[9]) * ym1);
+            xl0 = T(sc[0]) * q0 + T(sc[1]) * q1;
+            xl1 = T(sc[2]) * q0 + T(sc[3]) * q1;
+        } else {
+            // Sherman–Morrison
+            xl0 = (y1c + T(sc[0]) * g[0]) / T(sc[1]);
+            xl1 = T(0);
+        }
+        A.xl[sys * 2 + 0] = xl0;
+        A.xl[sys * 2 + 1] = xl1;
+    }
+}
+
 }  // namespace tp
 }  // namespace pb

@@ -20,20 +20,25 @@ if bench:
 launches = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "launch_summary.py"),
                            os.path.join(g, "launches.csv")], capture_output=True, text=True).stdout
 open(os.path.join(out, f"{tag}_launches.txt"), "w").write(launches)
-rows = []
+rows, adi_rows = [], []
 for rep in ("prof_band.ncu-rep", "prof_adi.ncu-rep"):
     p = os.path.join(g, rep)
     if os.path.exists(p):
-        rows += ncu_summary.summarise(p)
+        got = ncu_summary.summarise(p)
+        for r in got:
+            r["capture"] = "pent_solve cfg2" if rep == "prof_band.ncu-rep" else "one ch_adi_step cfg4"
+        rows += got
+        if rep == "prof_adi.ncu-rep":
+            adi_rows = got
 with open(os.path.join(out, f"{tag}_ncu_full.jsonl"), "w") as f:
     for r in rows:
         f.write(json.dumps(r) + "\n")
 traffic = {}
 for r in rows:
     t = r.get("dram_read", 0) + r.get("dram_write", 0)
-    if "tp_" in r["kernel"]:   # pass 1 + scan + pass 2 of one pent_solve
+    if r["capture"] == "pent_solve cfg2":   # pass 1 + scan + pass 2 of one pent_solve
         traffic["pent_solve_f64"] = traffic.get("pent_solve_f64", 0) + t
-    if "adi_pass" in r["kernel"]:
+    else:                                   # pass A + y-sweep (3 kernels) + combine of one step
         traffic["adi_step_f64"] = traffic.get("adi_step_f64", 0) + t
 json.dump(traffic, open(os.path.join(out, "ncu_traffic.json"), "w"), indent=1)
 print(launches)
