@@ -113,6 +113,23 @@ static int64_t tp_slab_systems(int64_t M, int64_t n, int64_t count, size_t es)
     return ms >= M ? M : ms;
 }
 
+// launch with programmatic stream serialization (see pdl_wait in twopass.cuh)
+template <typename Kern, typename... Args>
+static cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <typename T, int K, bool PER, bool P2>
 static int tp_pass_prep(size_t *smem)
 {
@@ -202,16 +219,21 @@ static int launch_tp_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
         A.G = (int)((A.ms + tp::TW - 1) / tp::TW);
         const int64_t ntile = (int64_t)nq * A.G * count;
         const unsigned grid = (unsigned)(ntile < nsm ? ntile : nsm);
-        tp::tp_pass_kernel<T, K, PER, false><<<grid, 32 * (tp::NWC1 + 1), sm1, st>>>(tmap, smap, A);
+        PB_CUDA_TRY(launch_pdl(tp::tp_pass_kernel<T, K, PER, false>, dim3(grid), dim3(32 * (tp::NWC1 + 1)), sm1, st, tmap,
+                               smap, A));
         PB_LAUNCH_CHECK();
         if (nq <= tp::SEQ_MAX)
-            tp::tp_scan_seq_kernel<T, K, PER><<<(unsigned)((nsys + 255) / 256), 256, 0, st>>>(A);
+            PB_CUDA_TRY(launch_pdl(tp::tp_scan_seq_kernel<T, K, PER>, dim3((unsigned)((nsys + 255) / 256)), dim3(256), 0,
+                                   st, A));
         else if (nq <= tp::NSEG_R * tp::CPS_R)
-            tp::tp_scan_reg_kernel<T, K, PER><<<(unsigned)(nsys / tp::TW), 32 * tp::NSEG_R, 0, st>>>(A);
+            PB_CUDA_TRY(launch_pdl(tp::tp_scan_reg_kernel<T, K, PER>, dim3((unsigned)(nsys / tp::TW)),
+                                   dim3(32 * tp::NSEG_R), 0, st, A));
         else
-            tp::tp_scan_kernel<T, K, PER><<<(unsigned)(nsys / tp::TW), 32 * tp::NSEG, 0, st>>>(A);
+            PB_CUDA_TRY(launch_pdl(tp::tp_scan_kernel<T, K, PER>, dim3((unsigned)(nsys / tp::TW)), dim3(32 * tp::NSEG),
+                                   0, st, A));
         PB_LAUNCH_CHECK();
-        tp::tp_pass_kernel<T, K, PER, true><<<grid, 32 * (tp::NWC + 1), sm2, st>>>(tmap, smap, A);
+        PB_CUDA_TRY(launch_pdl(tp::tp_pass_kernel<T, K, PER, true>, dim3(grid), dim3(32 * (tp::NWC + 1)), sm2, st, tmap,
+                               smap, A));
         PB_LAUNCH_CHECK();
     }
     PB_CUDA_TRY(cudaEventRecord(P.done, st));

@@ -148,6 +148,12 @@ __device__ __forceinline__ void tma_store(const CUtensorMap *m, int c0, int c1, 
                  : "memory");
 }
 __device__ __forceinline__ uint32_t up16(uint32_t b) { return (b + 15u) & ~15u; }
+// programmatic dependent launch: the three kernels of a solve are launched with
+// programmatic stream serialization; each waits for its predecessor's memory
+// before touching shared data and lets its successor launch right away (the
+// successor's CTAs cannot be resident until this grid's CTAs leave anyway)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 struct TileId {
     int q, b, g;
@@ -283,6 +289,8 @@ __global__ void __launch_bounds__(32 * (nwc<P2>() + 1), 1) tp_pass_kernel(const 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    pdl_wait();
+    pdl_trigger();
 
     constexpr int NC = nwc<P2>();
     if (warp == NC) {
@@ -458,6 +466,8 @@ __device__ __forceinline__ void st_rec(T *p, const T *r)
 template <typename T, int K, bool PER>
 __global__ void __launch_bounds__(32 * NSEG) tp_scan_kernel(const Args<T> A)
 {
+    pdl_wait();
+    pdl_trigger();
     __shared__ ScanSmem<T> S;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t nsys = A.msp * A.count;
@@ -628,6 +638,8 @@ __device__ __forceinline__ void ldm4s(const T *p, T *m)
 template <typename T, int K, bool PER>
 __global__ void __launch_bounds__(32 * NSEG_R) tp_scan_reg_kernel(const Args<T> A)
 {
+    pdl_wait();
+    pdl_trigger();
     constexpr int NW = NSEG_R, CPS = CPS_R;
     __shared__ ScanSmem<T, NW> S;
     __shared__ __align__(16) T cts[NW * CPS][12];   // the chunk maps, staged once per CTA
@@ -764,6 +776,8 @@ constexpr int SEQ_MAX = 16;
 template <typename T, int K, bool PER>
 __global__ void __launch_bounds__(256) tp_scan_seq_kernel(const Args<T> A)
 {
+    pdl_wait();
+    pdl_trigger();
     __shared__ __align__(16) T cts[SEQ_MAX][12];
     const int nq = A.nq;
     for (int e = threadIdx.x; e < nq * 12; e += blockDim.x) (&cts[0][0])[e] = A.ct[e];
