@@ -49,8 +49,14 @@ constexpr int ADI_IB = 32;  // stencil column block
 
 __device__ __forceinline__ int64_t wrapi(int64_t x, int64_t n)
 {
-    while (x < 0) x += n;
-    while (x >= n) x -= n;
+    // one conditional step covers the stencil halos (|offset| <= 2 + a column block)
+    // when n >= the column block; the loops only run for tiny grids
+    x = x < 0 ? x + n : x;
+    x = x >= n ? x - n : x;
+    if ((uint64_t)x >= (uint64_t)n) {
+        while (x < 0) x += n;
+        while (x >= n) x -= n;
+    }
     return x;
 }
 
