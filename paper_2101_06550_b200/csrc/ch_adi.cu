@@ -90,15 +90,31 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) adi_pass_a(const AdiA
         const int64_t i0 = ib0 + ib;
         const bool live = i0 < n;  // CTA-uniform
         if (live) {
-            for (int e = tid; e < (W + 4) * SB; e += NT) {
-                const int r = e / SB, q = e % SB;
-                // periodic in j (whole grid), or halo rows of a row block (ext)
-                const int64_t jr = EXT ? (j0 + r < rows + 3 ? j0 + r : rows + 3) : wrapi(j0 - 2 + r, n);
-                const int64_t idx = jr * n + wrapi(i0 - 2 + q, n);
-                const T cnv = __ldg(Cn + idx), cmv = __ldg(Cm + idx);
-                cb[e] = T(2) * cnv - cmv;
-                if (r >= 1 && r < W + 3 && q >= 1 && q < IB + 3) nl[(r - 1) * SN + (q - 1)] = cnv * cnv * cnv - cnv;
-                if (r >= 2 && r < W + 2 && q >= 2 && q < IB + 2) dl[(r - 2) * IB + (q - 2)] = cnv - cmv;
+            // all of this thread's staging loads first (latency overlap), then the stores
+            constexpr int NST = ((W + 4) * SB + NT - 1) / NT;
+            T cnr[NST], cmr[NST];
+#pragma unroll
+            for (int u = 0; u < NST; ++u) {
+                const int e = tid + u * NT;
+                if (e < (W + 4) * SB) {
+                    const int r = e / SB, q = e % SB;
+                    // periodic in j (whole grid), or halo rows of a row block (ext)
+                    const int64_t jr = EXT ? (j0 + r < rows + 3 ? j0 + r : rows + 3) : wrapi(j0 - 2 + r, n);
+                    const int64_t idx = jr * n + wrapi(i0 - 2 + q, n);
+                    cnr[u] = __ldg(Cn + idx);
+                    cmr[u] = __ldg(Cm + idx);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < NST; ++u) {
+                const int e = tid + u * NT;
+                if (e < (W + 4) * SB) {
+                    const int r = e / SB, q = e % SB;
+                    const T cnv = cnr[u], cmv = cmr[u];
+                    cb[e] = T(2) * cnv - cmv;
+                    if (r >= 1 && r < W + 3 && q >= 1 && q < IB + 3) nl[(r - 1) * SN + (q - 1)] = cnv * cnv * cnv - cnv;
+                    if (r >= 2 && r < W + 2 && q >= 2 && q < IB + 2) dl[(r - 2) * IB + (q - 2)] = cnv - cmv;
+                }
             }
         }
         __syncthreads();
