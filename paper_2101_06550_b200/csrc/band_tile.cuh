@@ -258,6 +258,7 @@ int stream_max_ctas_f32(int K, int periodic);
 int twopass_build_tables(Band *h, cudaStream_t st);
 int launch_tp_f64(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st);
 int launch_tp_f32(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st);
+int launch_tp_m(const Band *h, void *x, int64_t M, cudaStream_t st);
 
 // per-(dtype, K) entry points, defined in banded_inst_*.cu
 int launch_tile_f64_k2(const Band *h, void *x, int layout, int64_t count, int64_t bstride, cudaStream_t st);

@@ -783,7 +783,9 @@ static int solve_impl(const Band *h, void *rhs, int layout, int64_t count, int64
     const bool want_tile = solver && !strcmp(solver, "tile");
     const bool want_clu = solver && !strcmp(solver, "cluster");
     const bool inter = h->shared() && layout == PB_INTERLEAVED && al;
-    if (inter && !want_stream && !want_tile && !want_clu && h->tplan.ok)
+    // (count > 1 stays off the two-pass path: batched launches faulted
+    // intermittently there under sustained back-to-back solves, tools/iso_stress.sh)
+    if (inter && !want_stream && !want_tile && !want_clu && h->tplan.ok && count == 1)
         rc = h->dtype == PB_F64 ? launch_tp_f64(h, sx.dev, count, bstride, st)
                                 : launch_tp_f32(h, sx.dev, count, bstride, st);
     else if (inter && want_stream && h->splan.ok)

@@ -43,6 +43,10 @@ struct AdiArgs {
     // rows + 4 rows (2 halo rows above and below, no wrap in j); w holds `rows`
     int64_t rows = 0;
     int ext = 0;
+    // w layout: 0 = [sim][j][i]; else w[(j * wperm + sim) * n + i] with wperm = sims
+    // (all simulations' columns of one grid row contiguous: the y-sweep is then ONE
+    // batch of sims * n interleaved systems)
+    int64_t wperm = 0;
 };
 
 constexpr int ADI_IB = 32;  // stencil column block
@@ -81,7 +85,8 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) adi_pass_a(const AdiA
     const int64_t plane_in = (EXT ? rows + 4 : n) * n, plane_w = rows * n;
     const T *Cn = A.cn + (int64_t)blockIdx.y * plane_in;
     const T *Cm = A.cm + (int64_t)blockIdx.y * plane_in;
-    T *Wo = A.w + (int64_t)blockIdx.y * plane_w;
+    T *Wo = A.w + (int64_t)blockIdx.y * (A.wperm ? n : plane_w);
+    const int64_t wrs = A.wperm ? A.wperm * n : n;   // w row stride
     const int64_t ib0 = (int64_t)c * RC;  // first solve row (grid column i) of this CTA
     const T *cs = A.core.coef + ib0 * COEF_STRIDE;
 
@@ -147,7 +152,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) adi_pass_a(const AdiA
     for (int e = tid; e < W * RC; e += NT) {
         const int jj = e / RC, ii = e % RC;
         const int64_t j = j0 + jj, i = ib0 + ii;
-        if (j < rows && i < n) __stcg(Wo + j * n + i, tile[ii * WP + jj]);
+        if (j < rows && i < n) __stcg(Wo + j * wrs + i, tile[ii * WP + jj]);
     }
 }
 
@@ -346,6 +351,30 @@ __global__ void adi_combine_kernel(int64_t count, const T *__restrict__ cn, T *_
         cm[k] = (T(2) * cn[k] - cm[k]) + v[k];
 }
 
+// the same combine with v in the permuted layout v[(j * sims + sim) * n + i]
+template <typename T>
+__global__ void adi_combine_perm_kernel(int64_t sims, int64_t n, const T *__restrict__ cn, T *__restrict__ cm,
+                                        const T *__restrict__ v)
+{
+    using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+    constexpr int E = 16 / sizeof(T);
+    const int64_t nr = n / E, rows = sims * n;   // vectors per grid row; grid rows (sim, j)
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < rows * nr; k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = k / nr, iv = k - row * nr, sim = row / n, j = row - sim * n;
+        const V *a = reinterpret_cast<const V *>(cn + row * n) + iv;
+        V *b = reinterpret_cast<V *>(cm + row * n) + iv;
+        const V *c = reinterpret_cast<const V *>(v + (j * sims + sim) * n) + iv;
+        const V x = __ldcs(a), y = __ldcs(b), z = __ldcs(c);
+        V o;
+        const T *xs = reinterpret_cast<const T *>(&x), *ys = reinterpret_cast<const T *>(&y),
+                *zs = reinterpret_cast<const T *>(&z);
+        T *os = reinterpret_cast<T *>(&o);
+#pragma unroll
+        for (int e = 0; e < E; ++e) os[e] = (T(2) * xs[e] - ys[e]) + zs[e];
+        __stcs(b, o);
+    }
+}
+
 template <typename T>
 static int adi_run(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nsteps, cudaStream_t st)
 {
@@ -374,6 +403,7 @@ static int adi_run(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nst
     const bool ysweep_tp = h->tplan.ok && !(ys && !strcmp(ys, "band")) && (n * (int64_t)sizeof(T)) % 16 == 0 &&
                            (uintptr_t)s->work % 16 == 0 && (uintptr_t)s->c_cur % 16 == 0 &&
                            (uintptr_t)s->c_prev % 16 == 0;
+    A.wperm = ysweep_tp ? s->sims : 0;
     for (int64_t step = 0; step < nsteps; ++step) {
         A.cn = (const T *)s->c_cur;
         A.cm = (T *)s->c_prev;
@@ -381,12 +411,12 @@ static int adi_run(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nst
         if (ysweep_tp) {
             // y-sweep = the batched interleaved solve (systems = columns i, one batch
             // per simulation) by the two-pass TMA solve, then the C^{n+1} combine
-            rc = sizeof(T) == 8 ? launch_tp_f64(h, A.w, s->sims, n * n, st) : launch_tp_f32(h, A.w, s->sims, n * n, st);
-            if (rc) return rc;
+            // (w is in the permuted layout: one batch of sims * n systems)
+            if ((rc = launch_tp_m(h, A.w, s->sims * n, st))) return rc;
             int dev = 0, nsm = 0;
             PB_CUDA_TRY(cudaGetDevice(&dev));
             PB_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-            adi_combine_kernel<T><<<(unsigned)(nsm * 8), 256, 0, st>>>(s->sims * n * n, A.cn, A.cm, A.w);
+            adi_combine_perm_kernel<T><<<(unsigned)(nsm * 8), 256, 0, st>>>(s->sims, n, A.cn, A.cm, A.w);
             PB_LAUNCH_CHECK();
         } else if ((rc = launch_adi_cfg<T>(h, A, s->sims, st, false))) {
             return rc;

@@ -140,9 +140,9 @@ static int tp_pass_prep(size_t *smem)
 }
 
 template <typename T, int K, bool PER>
-static int launch_tp_t(const Band *h, T *x, int64_t count, int64_t bstride, cudaStream_t st)
+static int launch_tp_t(const Band *h, T *x, int64_t count, int64_t bstride, cudaStream_t st, int64_t Mo = 0)
 {
-    const int64_t M = h->batch, n = h->n;
+    const int64_t M = Mo > 0 ? Mo : h->batch, n = h->n;
     const int nq = h->tplan.nq;
     const int64_t ms = tp_slab_systems(M, n, count, sizeof(T));
     const int64_t msp = (ms + tp::TW - 1) / tp::TW * tp::TW;
@@ -160,9 +160,15 @@ static int launch_tp_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
     // stores: box (128 bytes of systems, 64 rows).  OOB loads zero-fill, OOB
     // stores are clipped (ragged M and n)
     CUtensorMap tmap, smap;
+    bool flat = false;
     {
         const int64_t bs = count > 1 ? bstride : M * n;
-        cuuint64_t dims[3] = {(cuuint64_t)M, (cuuint64_t)n, (cuuint64_t)count};
+        // contiguous batches whose systems are whole chunks: one 2-D (M, n*count) view
+        // (3-D maps with count > 1 faulted intermittently under sustained
+        // back-to-back solves, tools/iso_stress.sh)
+        flat = count > 1 && bs == M * n && n % tp::Q == 0 && n * count < (int64_t)1 << 31;
+        const int rank = flat ? 2 : 3;
+        cuuint64_t dims[3] = {(cuuint64_t)M, (cuuint64_t)(flat ? n * count : n), (cuuint64_t)(flat ? 1 : count)};
         cuuint64_t strides[2] = {(cuuint64_t)(M * sizeof(T)), (cuuint64_t)(bs * sizeof(T))};
         cuuint32_t box[3] = {(cuuint32_t)tp::TW, (cuuint32_t)tp::Q, 1};
         cuuint32_t sbox[3] = {(cuuint32_t)(128 / sizeof(T)), (cuuint32_t)tp::Q, 1};
@@ -170,10 +176,10 @@ static int launch_tp_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
         auto enc = tensor_map_encoder();
         if (!enc) return set_error(PB_ECUDA, "cuTensorMapEncodeTiled unavailable");
         const auto dt = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-        CUresult r = enc(&tmap, dt, 3, (void *)x, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CUresult r = enc(&tmap, dt, rank, (void *)x, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r == CUDA_SUCCESS)
-            r = enc(&smap, dt, 3, (void *)x, dims, strides, sbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            r = enc(&smap, dt, rank, (void *)x, dims, strides, sbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return set_error(PB_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     }
@@ -191,6 +197,7 @@ static int launch_tp_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
     A.qspec = PER ? (int)(h->srow[0] / tp::Q) : nq;
     A.msp = msp;
     A.keep = ms < M;   // slabbed: the slab is sized to stay in L2 until pass 2
+    A.flat = flat ? 1 : 0;
 
 
     // per-handle scratch for one slab (reused by the slabs in stream order);
@@ -222,7 +229,7 @@ static int launch_tp_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
         PB_CUDA_TRY(launch_pdl(tp::tp_pass_kernel<T, K, PER, false>, dim3(grid), dim3(32 * (tp::NWC1 + 1)), sm1, st, tmap,
                                smap, A));
         PB_LAUNCH_CHECK();
-        if (nq <= tp::SEQ_MAX)
+            if (nq <= tp::SEQ_MAX)
             PB_CUDA_TRY(launch_pdl(tp::tp_scan_seq_kernel<T, K, PER>, dim3((unsigned)((nsys + 255) / 256)), dim3(256), 0,
                                    st, A));
         else if (nq <= tp::NSEG_R * tp::CPS_R)
@@ -241,14 +248,21 @@ static int launch_tp_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
 }
 
 template <typename T>
-static int launch_tp_dt(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st)
+static int launch_tp_dt(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st, int64_t Mo = 0)
 {
     T *X = (T *)x;
     if (h->K == 2)
-        return h->periodic ? launch_tp_t<T, 2, true>(h, X, count, bstride, st)
-                           : launch_tp_t<T, 2, false>(h, X, count, bstride, st);
-    return h->periodic ? launch_tp_t<T, 1, true>(h, X, count, bstride, st)
-                       : launch_tp_t<T, 1, false>(h, X, count, bstride, st);
+        return h->periodic ? launch_tp_t<T, 2, true>(h, X, count, bstride, st, Mo)
+                           : launch_tp_t<T, 2, false>(h, X, count, bstride, st, Mo);
+    return h->periodic ? launch_tp_t<T, 1, true>(h, X, count, bstride, st, Mo)
+                       : launch_tp_t<T, 1, false>(h, X, count, bstride, st, Mo);
+}
+
+// one batch of M systems sharing the handle's LHS (M need not equal h->batch)
+int launch_tp_m(const Band *h, void *x, int64_t M, cudaStream_t st)
+{
+    return h->dtype == PB_F64 ? launch_tp_dt<double>(h, x, 1, M * h->n, st, M)
+                              : launch_tp_dt<float>(h, x, 1, M * h->n, st, M);
 }
 
 int launch_tp_f64(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st)

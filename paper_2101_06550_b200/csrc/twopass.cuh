@@ -77,6 +77,7 @@ struct Args {
     int nq, count, G;        // chunks, batches, tiles across ms
     int qspec;               // first chunk holding a cyclic row (cyclic only)
     int keep;                // pass 1 loads with L2 evict_last (the slab fits in L2)
+    int flat;                // batches contiguous and n % Q == 0: 2-D maps, row = b * n + r
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -133,6 +134,20 @@ __device__ __forceinline__ void tma_load(void *dst, const CUtensorMap *m, int c0
         " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(su32(dst)),
         "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
         : "memory");
+}
+__device__ __forceinline__ void tma_load2(void *dst, const CUtensorMap *m, int c0, int c1, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)),
+        "l"(m), "r"(c0), "r"(c1), "r"(su32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store2(const CUtensorMap *m, int c0, int c1, const void *src)
+{
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(m), "r"(c0), "r"(c1),
+                 "r"(su32(src))
+                 : "memory");
 }
 __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
 {
@@ -316,7 +331,9 @@ __global__ void __launch_bounds__(32 * (nwc<P2>() + 1), 1) tp_pass_kernel(const 
             const int64_t sys0 = (int64_t)id.b * A.msp + (int64_t)id.g * TW;
             const int nt = (int)min((int64_t)TW, A.ms - (int64_t)id.g * TW);
             bar_expect_tx(&sm.full[sl], bytes);
-            if (hint)
+            if (A.flat)
+                tma_load2(slot, &tmap, (int)(A.s0 + (int64_t)id.g * TW), (int)((int64_t)id.b * A.n + r0), &sm.full[sl]);
+            else if (hint)
                 tma_load(slot, &tmap, (int)(A.s0 + (int64_t)id.g * TW), (int)r0, id.b, &sm.full[sl], pol);
             else
                 tma_load(slot, &tmap, (int)(A.s0 + (int64_t)id.g * TW), (int)r0, id.b, &sm.full[sl]);
@@ -399,7 +416,11 @@ __global__ void __launch_bounds__(32 * (nwc<P2>() + 1), 1) tp_pass_kernel(const 
         if (lane == 0) {
 #pragma unroll
             for (int h = 0; h < NSW; ++h)
-                tma_store(&smap, (int)(A.s0 + (int64_t)id.g * TW + h * SW), (int)r0, id.b, o + h * Q * SW);
+                if (A.flat)
+                    tma_store2(&smap, (int)(A.s0 + (int64_t)id.g * TW + h * SW), (int)((int64_t)id.b * A.n + r0),
+                               o + h * Q * SW);
+                else
+                    tma_store(&smap, (int)(A.s0 + (int64_t)id.g * TW + h * SW), (int)r0, id.b, o + h * Q * SW);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
         pend = true;
