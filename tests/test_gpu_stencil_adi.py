@@ -145,11 +145,12 @@ def test_table_3_1_on_gpu():
 
 @pytest.mark.parametrize("n,sims", [(64, 3), (100, 2), (512, 2)])
 def test_adi_ysweep_paths_agree(n, sims, monkeypatch):
-    """The y-sweep by the two-pass solve + combine (default) and by the fused
-    band_core pass B (PB_ADI_YSWEEP=band) give the same step to rounding."""
+    """The y-sweep by the two-pass solve + combine (PB_ADI_YSWEEP=tp) and by the
+    fused band_core pass B (default) give the same step to rounding."""
     L = n * synth.DX_STATS
     dt = synth.ch_dt(n, L)
     c0 = synth.ch_ic_random(sims, n, seed=9)
+    monkeypatch.setenv("PB_ADI_YSWEEP", "tp")
     a, _ = gpu_adi(c0, 3, dt=dt, L=L)
     monkeypatch.setenv("PB_ADI_YSWEEP", "band")
     b, _ = gpu_adi(c0, 3, dt=dt, L=L)
