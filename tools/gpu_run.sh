@@ -7,5 +7,5 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 --adi-steps 5 --no-cpu > gpurun_out/ncu_launch.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:tp_ -s 7 -c 3 -o gpurun_out/prof_band python bench.py --steps 3 --warmup 3 --no-cpu --no-adi --no-dist > gpurun_out/ncu_full1.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k 'regex:adi_pass_a|adi_combine|tp_pass|tp_scan' -s 5 -c 5 -o gpurun_out/prof_adi python tools/adi_sweep.py 512 > gpurun_out/ncu_full2.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k 'regex:adi_pass' -s 2 -c 2 -o gpurun_out/prof_adi python tools/adi_sweep.py 512 > gpurun_out/ncu_full2.log 2>&1
 ls -la gpurun_out

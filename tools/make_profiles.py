@@ -38,7 +38,7 @@ for r in rows:
     t = r.get("dram_read", 0) + r.get("dram_write", 0)
     if r["capture"] == "pent_solve cfg2":   # pass 1 + scan + pass 2 of one pent_solve
         traffic["pent_solve_f64"] = traffic.get("pent_solve_f64", 0) + t
-    else:                                   # pass A + y-sweep (3 kernels) + combine of one step
+    else:                                   # all kernels of one ADI step (pass A + pass B)
         traffic["adi_step_f64"] = traffic.get("adi_step_f64", 0) + t
 json.dump(traffic, open(os.path.join(out, "ncu_traffic.json"), "w"), indent=1)
 print(launches)
