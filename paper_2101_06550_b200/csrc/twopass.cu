@@ -159,8 +159,26 @@ static int launch_tp_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
     // tensor maps over x: dims (M, n, count).  Loads: box (32 systems, 64 rows);
     // stores: box (128 bytes of systems, 64 rows).  OOB loads zero-fill, OOB
     // stores are clipped (ragged M and n)
-    CUtensorMap tmap, smap;
-    bool flat = false;
+    CUtensorMap tmap, smap, cmap1, cmap2;
+    bool flat = false, cmaps_ok = false;
+    {
+        // coefficient rows as 2-D tensors: pass 1 rec (REC per row), pass 2 coef (COEF_STRIDE per row)
+        auto enc = tensor_map_encoder();
+        if (!enc) return set_error(PB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        const auto dt = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+        const int64_t rrows = (int64_t)nq * tp::Q;
+        cuuint64_t d1[2] = {(cuuint64_t)tp::REC, (cuuint64_t)rrows}, s1[1] = {(cuuint64_t)(tp::REC * sizeof(T))};
+        cuuint32_t b1[2] = {(cuuint32_t)tp::REC, (cuuint32_t)tp::Q}, e1[2] = {1, 1};
+        CUresult r = enc(&cmap1, dt, 2, (void *)h->tplan.rec, d1, s1, b1, e1, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        cuuint64_t d2[2] = {(cuuint64_t)COEF_STRIDE, (cuuint64_t)h->rows_alloc},
+                   s2[1] = {(cuuint64_t)(COEF_STRIDE * sizeof(T))};
+        cuuint32_t b2[2] = {(cuuint32_t)COEF_STRIDE, (cuuint32_t)tp::Q};
+        if (r == CUDA_SUCCESS)
+            r = enc(&cmap2, dt, 2, (void *)h->coef, d2, s2, b2, e1, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        cmaps_ok = r == CUDA_SUCCESS;   // (fp32 rec rows are 24 B: not a legal TMA row; bulk copies then)
+    }
     {
         const int64_t bs = count > 1 ? bstride : M * n;
         // contiguous batches whose systems are whole chunks: one 2-D (M, n*count) view
@@ -198,6 +216,7 @@ static int launch_tp_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
     A.msp = msp;
     A.keep = ms < M;   // slabbed: the slab is sized to stay in L2 until pass 2
     A.flat = flat ? 1 : 0;
+    const char *p2g_env = getenv("PB_TP_P2G");   // 0 bulk, 2 tensor; unset = auto
 
 
     // per-handle scratch for one slab (reused by the slabs in stream order);
@@ -225,9 +244,15 @@ static int launch_tp_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
         A.ms = (M - s0) < ms ? (M - s0) : ms;
         A.G = (int)((A.ms + tp::TW - 1) / tp::TW);
         const int64_t ntile = (int64_t)nq * A.G * count;
+        // coefficient rows per stage: 1-D bulk copy (fastest) unless more than 1024 tile
+        // groups share a chunk -- then every in-flight stage copies the same rows, the
+        // regime in which the bulk copies faulted -- where a 2-D tensor
+        // load of the rows is used instead (measured fault-free there)
+        A.p2g = p2g_env ? atoi(p2g_env) : (cmaps_ok && (int64_t)A.G * count > 1024 ? 2 : 0);
+        if (A.p2g == 2 && !cmaps_ok) A.p2g = 0;
         const unsigned grid = (unsigned)(ntile < nsm ? ntile : nsm);
         PB_CUDA_TRY(launch_pdl(tp::tp_pass_kernel<T, K, PER, false>, dim3(grid), dim3(32 * (tp::NWC1 + 1)), sm1, st, tmap,
-                               smap, A));
+                               smap, cmap1, A));
         PB_LAUNCH_CHECK();
             if (nq <= tp::SEQ_MAX)
             PB_CUDA_TRY(launch_pdl(tp::tp_scan_seq_kernel<T, K, PER>, dim3((unsigned)((nsys + 255) / 256)), dim3(256), 0,
@@ -240,7 +265,7 @@ static int launch_tp_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
                                    0, st, A));
         PB_LAUNCH_CHECK();
         PB_CUDA_TRY(launch_pdl(tp::tp_pass_kernel<T, K, PER, true>, dim3(grid), dim3(32 * (tp::NWC + 1)), sm2, st, tmap,
-                               smap, A));
+                               smap, cmap2, A));
         PB_LAUNCH_CHECK();
     }
     PB_CUDA_TRY(cudaEventRecord(P.done, st));

@@ -78,6 +78,7 @@ struct Args {
     int qspec;               // first chunk holding a cyclic row (cyclic only)
     int keep;                // pass 1 loads with L2 evict_last (the slab fits in L2)
     int flat;                // batches contiguous and n % Q == 0: 2-D maps, row = b * n + r
+    int p2g;                 // coefficient rows per stage: 0 = 1-D bulk copy, 2 = 2-D tensor load
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -232,16 +233,27 @@ __device__ __forceinline__ void tile_carry(const T *d, const T *c, int kmax, int
 // pass-2 tile column (registers): forward sweep from (y0, y1), back
 // substitution from (z0, z1), cyclic correction x - Z x_l.  FULL: kmax == Q,
 // no row guards (the ragged last chunk takes the guarded copy)
-template <typename T, int K, bool PER, bool FULL>
+template <bool GL, typename T>
+__device__ __forceinline__ void cld2(const T *p, T &a, T &b)
+{
+    if (GL) {
+        a = __ldg(p);
+        b = __ldg(p + 1);
+    } else {
+        lds2(p, a, b);
+    }
+}
+
+template <typename T, int K, bool PER, bool FULL, bool GL = false>
 __device__ __forceinline__ void tile_solve(T (&v)[Q], const T *c, int kmax, T y0, T y1, T z0, T z1, T xl0, T xl1)
 {
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
         if (FULL || k < kmax) {
             T f0, f1;
-            lds2(c + k * COEF_STRIDE, f0, f1);
+            cld2<GL>(c + k * COEF_STRIDE, f0, f1);
             T g = f0 * v[k] - f1 * y1;
-            if (K == 2) g -= c[k * COEF_STRIDE + 2] * y0;
+            if (K == 2) g -= (GL ? __ldg(c + k * COEF_STRIDE + 2) : c[k * COEF_STRIDE + 2]) * y0;
             y0 = y1;
             y1 = g;
             v[k] = g;
@@ -251,7 +263,7 @@ __device__ __forceinline__ void tile_solve(T (&v)[Q], const T *c, int kmax, T y0
     for (int k = Q - 1; k >= 0; --k) {
         if (FULL || k < kmax) {
             T b1, b2;
-            lds2(c + k * COEF_STRIDE + 4, b1, b2);
+            cld2<GL>(c + k * COEF_STRIDE + 4, b1, b2);
             T xx = v[k] - b1 * z0;
             if (K == 2) xx -= b2 * z1;
             z1 = z0;
@@ -264,7 +276,7 @@ __device__ __forceinline__ void tile_solve(T (&v)[Q], const T *c, int kmax, T y0
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
             T z1v, z2v;
-            lds2(c + k * COEF_STRIDE + 6, z1v, z2v);
+            cld2<GL>(c + k * COEF_STRIDE + 6, z1v, z2v);
             T o = v[k] - z1v * xl0;
             if (K == 2) o -= z2v * xl1;
             v[k] = o;
@@ -287,6 +299,7 @@ __device__ __forceinline__ void load_inflow(const Args<T> &A, int64_t t, int lan
 template <typename T, int K, bool PER, bool P2>
 __global__ void __launch_bounds__(32 * (nwc<P2>() + 1), 1) tp_pass_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                      const __grid_constant__ CUtensorMap smap,
+                                                                     const __grid_constant__ CUtensorMap cmap,
                                                                      const Args<T> A)
 {
     using S = PassSmem<T, P2>;
@@ -327,7 +340,7 @@ __global__ void __launch_bounds__(32 * (nwc<P2>() + 1), 1) tp_pass_kernel(const 
             T *slot = sm.slot[sl];
             uint32_t bytes = TILE * sizeof(T);
             const uint32_t cb = up16((uint32_t)(kmax * (P2 ? COEF_STRIDE : REC) * sizeof(T)));
-            bytes += cb;
+            bytes += A.p2g == 2 ? (uint32_t)(Q * (P2 ? COEF_STRIDE : REC) * sizeof(T)) : cb;
             const int64_t sys0 = (int64_t)id.b * A.msp + (int64_t)id.g * TW;
             const int nt = (int)min((int64_t)TW, A.ms - (int64_t)id.g * TW);
             bar_expect_tx(&sm.full[sl], bytes);
@@ -341,7 +354,10 @@ __global__ void __launch_bounds__(32 * (nwc<P2>() + 1), 1) tp_pass_kernel(const 
             // fourth bulk copy per stage made pass 2 hang or fault
             // intermittently on B200 (tools/tp_stress2.sh); the consumers
             // prefetch them with plain loads one tile ahead instead)
-            bulk_load(slot + TILE, P2 ? A.coef + r0 * COEF_STRIDE : A.rec + r0 * REC, cb, &sm.full[sl]);
+            if (A.p2g == 2)   // the chunk's coefficient rows by a 2-D tensor load (row records x Q rows)
+                tma_load2(slot + TILE, &cmap, 0, (int)r0, &sm.full[sl]);
+            else
+                bulk_load(slot + TILE, P2 ? A.coef + r0 * COEF_STRIDE : A.rec + r0 * REC, cb, &sm.full[sl]);
         }
         return;
     }
