@@ -249,10 +249,6 @@ static int launch_tp_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
         // regime in which the bulk copies faulted -- where a 2-D tensor
         // load of the rows is used instead (measured fault-free there)
         A.p2g = p2g_env ? atoi(p2g_env) : (cmaps_ok && (int64_t)A.G * count > 1024 ? 2 : 0);
-        {
-            const char *ge = getenv("PB_TP_GMAJ");
-            A.gmaj = ge ? atoi(ge) : 0;
-        }
         if (A.p2g == 2 && !cmaps_ok) A.p2g = 0;
         const unsigned grid = (unsigned)(ntile < nsm ? ntile : nsm);
         PB_CUDA_TRY(launch_pdl(tp::tp_pass_kernel<T, K, PER, false>, dim3(grid), dim3(32 * (tp::NWC1 + 1)), sm1, st, tmap,

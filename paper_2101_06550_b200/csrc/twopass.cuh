@@ -79,7 +79,6 @@ struct Args {
     int keep;                // pass 1 loads with L2 evict_last (the slab fits in L2)
     int flat;                // batches contiguous and n % Q == 0: 2-D maps, row = b * n + r
     int p2g;                 // coefficient rows per stage: 0 = 1-D bulk copy, 2 = 2-D tensor load
-    int gmaj;                // group-major tile order (tile_of)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -175,18 +174,9 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 struct TileId {
     int q, b, g;
 };
-__device__ __forceinline__ TileId tile_of(int64_t t, int G, int count, int nq = 0)
+__device__ __forceinline__ TileId tile_of(int64_t t, int G, int count)
 {
     TileId r;
-    if (nq > 0) {
-        // group-major order: consecutive tiles walk the chunks of one group, so the
-        // stages in flight spread over all chunks (many-groups-per-chunk shapes)
-        const int64_t grp = t / nq;
-        r.q = (int)(t - grp * nq);
-        r.b = (int)(grp / G);
-        r.g = (int)(grp - (int64_t)r.b * G);
-        return r;
-    }
     const int64_t per_q = (int64_t)G * count;
     r.q = (int)(t / per_q);
     const int64_t rem = t - (int64_t)r.q * per_q;
@@ -298,7 +288,7 @@ __device__ __forceinline__ void tile_solve(T (&v)[Q], const T *c, int kmax, T y0
 template <typename T, bool PER>
 __device__ __forceinline__ void load_inflow(const Args<T> &A, int64_t t, int lane, T (&r)[6])
 {
-    const TileId id = tile_of(t, A.G, A.count, A.gmaj ? A.nq : 0);
+    const TileId id = tile_of(t, A.G, A.count);
     const int64_t sys = (int64_t)id.b * A.msp + (int64_t)id.g * TW + lane;
     const T *p = A.car + ((int64_t)id.q * A.msp * A.count + sys) * 4;
     r[0] = __ldcg(p), r[1] = __ldcg(p + 1), r[2] = __ldcg(p + 2), r[3] = __ldcg(p + 3);
@@ -344,7 +334,7 @@ __global__ void __launch_bounds__(32 * (nwc<P2>() + 1), 1) tp_pass_kernel(const 
         for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x, ++j) {
             const int sl = j % NS;
             if (j >= NS) bar_wait(&sm.empty[sl], ((j / NS) - 1) & 1);
-            const TileId id = tile_of(t, A.G, A.count, A.gmaj ? A.nq : 0);
+            const TileId id = tile_of(t, A.G, A.count);
             const int64_t r0 = (int64_t)id.q * Q;
             const int kmax = (int)min((int64_t)Q, A.n - r0);
             T *slot = sm.slot[sl];
@@ -381,7 +371,7 @@ __global__ void __launch_bounds__(32 * (nwc<P2>() + 1), 1) tp_pass_kernel(const 
     for (int64_t t = blockIdx.x + (int64_t)warp * gridDim.x; t < ntile; t += tstep, j += NC) {
         const int sl = j % NS;
         bar_wait(&sm.full[sl], (j / NS) & 1);
-        const TileId id = tile_of(t, A.G, A.count, A.gmaj ? A.nq : 0);
+        const TileId id = tile_of(t, A.G, A.count);
         const int64_t r0 = (int64_t)id.q * Q;
         const int kmax = (int)min((int64_t)Q, A.n - r0);
         const T *d = sm.slot[sl];
