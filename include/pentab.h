@@ -18,9 +18,12 @@
  *    stream).  All device work is enqueued on it; hot-path calls
  *    (pent_solve, tri_solve, stencil_apply, ch_adi_step with device buffers)
  *    never synchronise the host.
- *  - Handles are LIBRARY-OWNED and freed by the matching *_destroy.  A
- *    factored handle is read-only, so concurrent solves on different streams
- *    are safe.
+ *  - Handles are LIBRARY-OWNED and freed by the matching *_destroy.  The
+ *    factors of a handle are read-only after *_factor; the solve's scratch
+ *    (carry records, counters) is allocated per (handle, stream) under a
+ *    per-handle lock, so concurrent solves with one handle -- from several
+ *    host threads and/or on several streams -- are safe.  Destroying a
+ *    handle while solves are queued on it is not (the caller orders that).
  *  - Inputs are never modified except the documented in-place outputs.
  *  - No CPU fallback: without a usable CUDA device every compute call
  *    returns PB_ECUDA.
@@ -184,7 +187,7 @@ PB_API int ch_adi_step(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t
  * is, per rank (the orchestration and the two all-to-all
  * transposes live in paper_2101_06550_b200/dist.py):
  *   halo rows -> ch_dist_pass_a (RHS + x-sweep) -> ch_dist_pack ->
- *   all-to-all -> pent_solve (y-sweep on the rank's n/P columns, interleaved)
+ *   all-to-all -> ch_dist_ysweep (y-sweep on the rank's n/P columns, interleaved)
  *   -> all-to-all -> ch_dist_combine (C^{n+1} = 2C^n - C^{n-1} + v).
  * The x-then-y order is the thesis's (reading r18); results equal the
  * single-grid ch_adi_step up to rounding.
@@ -203,6 +206,13 @@ PB_API int ch_dist_pass_a(int64_t rows, int64_t n, int dtype, const void *cn_ext
                           double dt, const pb_ch_params *p, void *stream);
 PB_API int ch_dist_pack(int64_t rows, int64_t n, int64_t parts, int dtype, const void *w, void *packed,
                         void *stream);
+/* ch_dist_ysweep: the y-sweep L_y v = w of the rank's column block,
+ *   in place: cols is [n][ncols] interleaved (ncols systems of length n, the
+ *   receive layout of the first all-to-all), solved with the cyclic L_y of
+ *   (n, dt, D, gamma, L) factored once and cached.  ncols * sizeof(T) must be
+ *   a multiple of 16 and cols 16-byte aligned (PB_EINVAL otherwise).       */
+PB_API int ch_dist_ysweep(int64_t ncols, int64_t n, int dtype, void *cols, double dt, const pb_ch_params *p,
+                          void *stream);
 PB_API int ch_dist_combine(int64_t rows, int64_t n, int64_t parts, int dtype, const void *cn_ext, void *cm_ext,
                            const void *v_packed, void *stream);
 

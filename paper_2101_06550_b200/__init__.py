@@ -23,7 +23,7 @@ PB_NONPERIODIC, PB_PERIODIC = 0, 1
 # every symbol include/pentab.h declares
 EXPORTS = ("pent_factor", "pent_solve", "pent_solve_many", "pent_destroy", "tri_factor", "tri_solve",
            "tri_destroy", "stencil_apply", "ch_workspace_bytes", "ch_adi_step", "ch_dist_pass_a",
-           "ch_dist_pack", "ch_dist_combine", "pb_last_error", "pb_launch_count", "pb_reset_launch_count",
+           "ch_dist_pack", "ch_dist_ysweep", "ch_dist_combine", "pb_last_error", "pb_launch_count", "pb_reset_launch_count",
            "pb_device_ok")
 
 
@@ -73,6 +73,7 @@ def lib() -> ctypes.CDLL:
         L.ch_adi_step.argtypes = [ctypes.POINTER(pb_ch_state), D, ctypes.POINTER(pb_ch_params), I64, P]
         L.ch_dist_pass_a.argtypes = [I64, I64, I, P, P, P, D, ctypes.POINTER(pb_ch_params), P]
         L.ch_dist_pack.argtypes = [I64, I64, I64, I, P, P, P]
+        L.ch_dist_ysweep.argtypes = [I64, I64, I, P, D, ctypes.POINTER(pb_ch_params), P]
         L.ch_dist_combine.argtypes = [I64, I64, I64, I, P, P, P, P]
         L.pb_last_error.argtypes = [ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.c_char_p, ctypes.c_size_t]
         L.pb_launch_count.restype = I64
@@ -262,6 +263,12 @@ def ch_dist_pass_a(cn_ext, cm_ext, w, *, rows, n, dt, D=1.0, gamma=0.01, L, stre
 
 def ch_dist_pack(w, packed, *, rows, n, parts, stream=None):
     _check(lib().ch_dist_pack(rows, n, parts, _dtype_code(w), _ptr(w), _ptr(packed), _stream(w, stream)))
+
+
+def ch_dist_ysweep(cols, *, ncols, n, dt, D=1.0, gamma=0.01, L, stream=None):
+    """y-sweep of the rank's [n][ncols] column block, in place (pentab.h)."""
+    p = pb_ch_params(D, gamma, L)
+    _check(lib().ch_dist_ysweep(ncols, n, _dtype_code(cols), _ptr(cols), dt, ctypes.byref(p), _stream(cols, stream)))
 
 
 def ch_dist_combine(cn_ext, cm_ext, v_packed, *, rows, n, parts, stream=None):

@@ -2,6 +2,9 @@
 // and its launcher; instantiated per (dtype, K) in banded_inst_*.cu so the
 // nvcc builds run in parallel.
 #pragma once
+#include <map>
+#include <mutex>
+
 #include "band_core.cuh"
 #include "common.cuh"
 
@@ -14,31 +17,24 @@ struct Plan {
     void *tab = nullptr, *mfc = nullptr, *mbc = nullptr;  // dtype scan tables (band_core.cuh)
 };
 
-// streaming two-phase solve plan (stream_solve.cuh): tables in dtype
-struct StreamPlan {
-    int ok = 0;
-    int nrb = 0, R = 0;
-    void *tab = nullptr, *mft = nullptr, *mbt = nullptr, *hft = nullptr, *gsp = nullptr, *rsp = nullptr;
-    int srb[4] = {-1, -1, -1, -1};
+// fused streaming solve plan (fused_solve.cuh): row records, chunk maps,
+// cyclic-row responses (dtype), and per-stream scratch.  Solves on different
+// streams get different scratch (concurrent solves with one handle are safe);
+// solves on one stream reuse theirs in stream order.
+struct FusedScratch {
+    void *buf = nullptr;
+    size_t bytes = 0;
+    unsigned epoch = 0;
+    int64_t nq = 0, nsys = 0;
+    // the last tensor map encoded for this stream (rhs pointer + shape key)
+    uint64_t key[6] = {0, 0, 0, 0, 0, 0};
+    alignas(64) unsigned char tmap[128];
 };
-
-// cluster solve plan (cluster_solve.cuh): chunk / CTA transfer matrices in dtype
-struct ClusterPlan {
-    int ok = 0, C = 0;
-    void *mf = nullptr, *mb = nullptr, *mfc = nullptr, *mbc = nullptr;
-    void *cc = nullptr;   // rows x 5 compact sweep coefficients (dtype)
-};
-
-// two-pass streaming solve plan (twopass.cuh): row records, chunk maps, cyclic-row responses (dtype)
-struct TwoPassPlan {
+struct FusedPlan {
     int ok = 0, nq = 0;
     void *rec = nullptr, *ct = nullptr, *rsp = nullptr;
-    // per-handle carry scratch (cudaMalloc, grow-only).  Solves on different
-    // streams are ordered through `done`.  (Bulk-async copies out of
-    // cudaMallocAsync pool memory intermittently faulted or hung on B200.)
-    mutable void *scratch = nullptr;
-    mutable size_t scratch_bytes = 0;
-    mutable cudaEvent_t done = nullptr;
+    mutable std::mutex mu;
+    mutable std::map<cudaStream_t, FusedScratch> scratch;
 };
 
 struct Band {
@@ -51,9 +47,7 @@ struct Band {
     void *coef = nullptr;     // dtype copy (== coefD for fp64)
     double *scal = nullptr;   // SCAL_LEN
     Plan plan;
-    StreamPlan splan;
-    ClusterPlan cplan;
-    TwoPassPlan tplan;
+    FusedPlan fplan;
     int64_t srow[4] = {-1, -1, -1, -1};
     // per-system LHS
     void *pcoef = nullptr;    // dtype, [(i*8 + j) * batch + s]
@@ -69,25 +63,13 @@ struct Band {
         cudaFree(plan.mbc);
         cudaFree(pcoef);
         cudaFree(pscal);
-        cudaFree(splan.tab);
-        cudaFree(splan.mft);
-        cudaFree(splan.mbt);
-        cudaFree(splan.hft);
-        cudaFree(splan.gsp);
-        cudaFree(splan.rsp);
-        cudaFree(cplan.mf);
-        cudaFree(cplan.mb);
-        cudaFree(cplan.mfc);
-        cudaFree(cplan.mbc);
-        cudaFree(cplan.cc);
-        cudaFree(tplan.rec);
-        cudaFree(tplan.ct);
-        cudaFree(tplan.rsp);
-        if (tplan.done) {
-            cudaEventSynchronize(tplan.done);
-            cudaEventDestroy(tplan.done);
+        cudaFree(fplan.rec);
+        cudaFree(fplan.ct);
+        cudaFree(fplan.rsp);
+        for (auto &kv : fplan.scratch) {
+            cudaStreamSynchronize(kv.first);
+            cudaFree(kv.second.buf);
         }
-        cudaFree(tplan.scratch);
     }
 };
 
@@ -240,25 +222,10 @@ static int launch_tile_l(const Band *h, T *x, int layout, int64_t count, int64_t
 
 int const_penta_band(int64_t n, double sigma, int dtype, int cfg, int C, cudaStream_t st, Band **out);
 
-// streaming solve (stream_solve_f64.cu / _f32.cu): geometry per dtype and launchers
-constexpr int STREAM_R = 256;          // max tile rows of the streaming solve (fp64 128, fp32 256)
-inline int stream_rows_per_tile(int dtype) { return dtype == PB_F64 ? 128 : 256; }
-constexpr int STREAM_MAX_NRB = 64;     // tiles per system the group scan supports
-int stream_build_tables(Band *h, cudaStream_t st);
-int launch_stream_f64(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st);
-int launch_stream_f32(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st);
-int stream_max_ctas_f64(int K, int periodic);
-int cluster_build_tables(Band *h, cudaStream_t st);
-int launch_clu_f64(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st);
-int launch_clu_f32(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st);
-int clu_max_clusters_f64(int C, int K, int periodic);
-int clu_max_clusters_f32(int C, int K, int periodic);
-constexpr int CLU_RC = 512;   // rows per CTA of the cluster solve
-int stream_max_ctas_f32(int K, int periodic);
-int twopass_build_tables(Band *h, cudaStream_t st);
-int launch_tp_f64(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st);
-int launch_tp_f32(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st);
-int launch_tp_m(const Band *h, void *x, int64_t M, cudaStream_t st);
+int fused_build_tables(Band *h, cudaStream_t st);
+// shared-LHS interleaved solve of `count` batches (batch k at x + k * bstride
+// elements); M = systems per batch (0: the handle's batch)
+int launch_fused(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st, int64_t M = 0);
 
 // per-(dtype, K) entry points, defined in banded_inst_*.cu
 int launch_tile_f64_k2(const Band *h, void *x, int layout, int64_t count, int64_t bstride, cudaStream_t st);

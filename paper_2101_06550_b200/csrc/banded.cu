@@ -320,60 +320,6 @@ __global__ void block_transfer_kernel(const double *mf, const double *mb, int C,
     }
 }
 
-// ---------------------------------------------------------------- streaming-solve tables
-// Tile-level matrices of the streaming solve (stream_solve.cuh), from the fp64
-// coefficients: for a tile of R rows, Mf_t maps the forward inflow
-// (g_{r0-2}, g_{r0-1}) to the outflow, Mb_t maps the backward inflow
-// (x_{r1}, x_{r1+1}) to (x_{r0}, x_{r0+1}), and Hf_t is the response of
-// (x_{r0}, x_{r0+1}) to the forward inflow (zero f, zero backward inflow).
-// gsp[j] is the response of g on spec row j to its tile's forward inflow.
-template <typename T>
-__global__ void tile_tables_kernel(const double *coef, int nrb, int R, int64_t s0, int64_t s1, int64_t s2, int64_t s3,
-                                   T *mft, T *mbt, T *hft, T *gsp, T *rsp)
-{
-    const int tile = blockIdx.x * blockDim.x + threadIdx.x;
-    if (tile >= nrb) return;
-    const int64_t r0 = (int64_t)tile * R;
-    const int64_t srow[4] = {s0, s1, s2, s3};
-    const double *cr = coef + r0 * COEF_STRIDE;
-    T *rf = rsp + (int64_t)tile * 4 * R;   // [RF0, RF1, RB0, RB1][R]
-    for (int col = 0; col < 2; ++col) {
-        // forward from the unit inflow, f = 0; then back substitution, zero backward inflow
-        double g[STREAM_R];
-        double y0 = col == 0, y1 = col == 1;
-        for (int k = 0; k < R; ++k) {
-            const double gg = -cr[k * 8 + 1] * y1 - cr[k * 8 + 2] * y0;
-            y0 = y1;
-            y1 = gg;
-            g[k] = gg;
-            for (int j = 0; j < 4; ++j)
-                if (srow[j] == r0 + k) gsp[j * 2 + col] = (T)gg;
-        }
-        mft[tile * 4 + 0 + col] = (T)y0;
-        mft[tile * 4 + 2 + col] = (T)y1;
-        double z0 = 0, z1 = 0;
-        for (int k = R - 1; k >= 0; --k) {
-            const double x = g[k] - cr[k * 8 + 4] * z0 - cr[k * 8 + 5] * z1;
-            z1 = z0;
-            z0 = x;
-            rf[col * R + k] = (T)x;
-        }
-        hft[tile * 4 + 0 + col] = (T)z0;
-        hft[tile * 4 + 2 + col] = (T)z1;
-        // back substitution of zero from the unit backward inflow
-        z0 = col == 0;
-        z1 = col == 1;
-        for (int k = R - 1; k >= 0; --k) {
-            const double x = -cr[k * 8 + 4] * z0 - cr[k * 8 + 5] * z1;
-            z1 = z0;
-            z0 = x;
-            rf[(2 + col) * R + k] = (T)x;
-        }
-        mbt[tile * 4 + 0 + col] = (T)z0;
-        mbt[tile * 4 + 2 + col] = (T)z1;
-    }
-}
-
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
 {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -387,108 +333,6 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
         cudaGetLastError();
     });
     return fn;
-}
-
-// Build the streaming plan of a shared-LHS handle (coefD factored, srow set).
-// Leaves splan.ok = 0 (other kernels serve the solve) when the tiles of one
-// system would not fit in the resident persistent grid.
-int stream_build_tables(Band *h, cudaStream_t st)
-{
-    const bool f64 = h->dtype == PB_F64;
-    const int R = stream_rows_per_tile(h->dtype);
-    const int64_t nrb = (h->n + R - 1) / R;
-    const int maxc = f64 ? stream_max_ctas_f64(h->K, h->periodic) : stream_max_ctas_f32(h->K, h->periodic);
-    h->splan.ok = 0;
-    if (maxc <= 0 || nrb > maxc || nrb > STREAM_MAX_NRB || h->rows_alloc < nrb * R || !tensor_map_encoder())
-        return PB_OK;
-    const size_t es = dtype_size(h->dtype);
-    PB_CUDA_TRY(cudaMalloc(&h->splan.mft, es * 4 * nrb));
-    PB_CUDA_TRY(cudaMalloc(&h->splan.mbt, es * 4 * nrb));
-    PB_CUDA_TRY(cudaMalloc(&h->splan.hft, es * 4 * nrb));
-    PB_CUDA_TRY(cudaMalloc(&h->splan.gsp, es * 8));
-    PB_CUDA_TRY(cudaMalloc(&h->splan.rsp, es * 4 * R * nrb));
-    PB_CUDA_TRY(cudaMemsetAsync(h->splan.gsp, 0, es * 8, st));
-    const unsigned gt = (unsigned)((nrb + 63) / 64);
-    if (f64)
-        tile_tables_kernel<double><<<gt, 64, 0, st>>>(h->coefD, (int)nrb, R, h->srow[0], h->srow[1], h->srow[2],
-                                                      h->srow[3], (double *)h->splan.mft, (double *)h->splan.mbt,
-                                                      (double *)h->splan.hft, (double *)h->splan.gsp,
-                                                      (double *)h->splan.rsp);
-    else
-        tile_tables_kernel<float><<<gt, 64, 0, st>>>(h->coefD, (int)nrb, R, h->srow[0], h->srow[1], h->srow[2],
-                                                     h->srow[3], (float *)h->splan.mft, (float *)h->splan.mbt,
-                                                     (float *)h->splan.hft, (float *)h->splan.gsp,
-                                                     (float *)h->splan.rsp);
-    PB_LAUNCH_CHECK();
-    for (int j = 0; j < 4; ++j) h->splan.srb[j] = h->srow[j] >= 0 ? (int)(h->srow[j] / R) : -1;
-    h->splan.nrb = (int)nrb;
-    h->splan.R = R;
-    h->splan.ok = 1;
-    return PB_OK;
-}
-
-// Plan of the cluster solve (cluster_solve.cuh): C = ceil(n / 512) CTAs per
-// group (<= 16), chunk transfer matrices (32 rows) and CTA block matrices.
-template <typename T>
-__global__ void compact_coef_kernel(const double *coef, int64_t rows, T *cc)
-{
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * 5; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / 5;
-        const int j = (int)(i % 5);
-        cc[i] = (T)coef[r * COEF_STRIDE + (j < 3 ? j : j + 1)];
-    }
-}
-
-__global__ void cast_f64_kernel(const double *src, float *dst, int64_t count)
-{
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
-        dst[i] = (float)src[i];
-}
-
-int cluster_build_tables(Band *h, cudaStream_t st)
-{
-    const bool f64 = h->dtype == PB_F64;
-    const int C = (int)((h->n + CLU_RC - 1) / CLU_RC);
-    h->cplan.ok = 0;
-    if (C > 16 || h->rows_alloc < (int64_t)C * CLU_RC || !tensor_map_encoder()) return PB_OK;
-    const int ncl = f64 ? clu_max_clusters_f64(C, h->K, h->periodic) : clu_max_clusters_f32(C, h->K, h->periodic);
-    if (ncl < 1) return PB_OK;
-    const size_t es = dtype_size(h->dtype);
-    const int64_t nch = (int64_t)C * (CLU_RC / 32);
-    double *mfD = nullptr, *mbD = nullptr;
-    PB_CUDA_TRY(cudaMallocAsync(&mfD, sizeof(double) * 4 * nch, st));
-    PB_CUDA_TRY(cudaMallocAsync(&mbD, sizeof(double) * 4 * nch, st));
-    PB_CUDA_TRY(cudaMalloc(&h->cplan.mf, es * 4 * nch));
-    PB_CUDA_TRY(cudaMalloc(&h->cplan.mb, es * 4 * nch));
-    PB_CUDA_TRY(cudaMalloc(&h->cplan.mfc, es * 4 * 16));
-    PB_CUDA_TRY(cudaMalloc(&h->cplan.mbc, es * 4 * 16));
-    PB_CUDA_TRY(cudaMalloc(&h->cplan.cc, es * 5 * (int64_t)C * CLU_RC));
-    if (f64)
-        compact_coef_kernel<double><<<64, 256, 0, st>>>(h->coefD, (int64_t)C * CLU_RC, (double *)h->cplan.cc);
-    else
-        compact_coef_kernel<float><<<64, 256, 0, st>>>(h->coefD, (int64_t)C * CLU_RC, (float *)h->cplan.cc);
-    PB_LAUNCH_CHECK();
-    transfer_kernel<<<(unsigned)((nch + 127) / 128), 128, 0, st>>>(h->coefD, nch, 32, mfD, mbD);
-    PB_LAUNCH_CHECK();
-    if (f64) {
-        PB_CUDA_TRY(cudaMemcpyAsync(h->cplan.mf, mfD, sizeof(double) * 4 * nch, cudaMemcpyDeviceToDevice, st));
-        PB_CUDA_TRY(cudaMemcpyAsync(h->cplan.mb, mbD, sizeof(double) * 4 * nch, cudaMemcpyDeviceToDevice, st));
-        block_transfer_kernel<double><<<1, 32, 0, st>>>(mfD, mbD, C, CLU_RC / 32, (double *)h->cplan.mfc,
-                                                       (double *)h->cplan.mbc);
-    } else {
-        cast_f64_kernel<<<16, 256, 0, st>>>(mfD, (float *)h->cplan.mf, 4 * nch);
-        PB_LAUNCH_CHECK();
-        cast_f64_kernel<<<16, 256, 0, st>>>(mbD, (float *)h->cplan.mb, 4 * nch);
-        PB_LAUNCH_CHECK();
-        block_transfer_kernel<float><<<1, 32, 0, st>>>(mfD, mbD, C, CLU_RC / 32, (float *)h->cplan.mfc,
-                                                      (float *)h->cplan.mbc);
-    }
-    PB_LAUNCH_CHECK();
-    PB_CUDA_TRY(cudaFreeAsync(mfD, st));
-    PB_CUDA_TRY(cudaFreeAsync(mbD, st));
-    h->cplan.C = C;
-    h->cplan.ok = 1;
-    return PB_OK;
 }
 
 // ---------------------------------------------------------------- one thread per system
@@ -561,18 +405,6 @@ static int choose_cfg(int64_t n, int64_t batch, int dtype, int *C_out)
 {
     const TileCfg *T = dtype == PB_F64 ? CFG64 : CFG32;
     const int W = dtype == PB_F64 ? 16 : 32;
-    const char *env = getenv("PB_TILE_CFG");
-    if (env) {
-        int k = atoi(env);
-        if (k >= 0 && k < NCFG) {
-            int64_t rc = (int64_t)(T[k].nt / W) * T[k].mr;
-            int64_t C = (n + rc - 1) / rc;
-            if (C <= MAX_CLUSTER) {
-                *C_out = (int)C;
-                return k;
-            }
-        }
-    }
     const int64_t groups = (batch + W - 1) / W;
     int best = -1;
     int64_t best_ctas = -1;
@@ -658,10 +490,6 @@ static int factor_impl(Band *h, const double *a, const double *b, const double *
         }
         h->rows_alloc = k >= 0 ? (int64_t)C * rc_rows : n;
         if (h->rows_alloc < n) h->rows_alloc = n;
-        const int64_t stream_rows = (n + STREAM_R - 1) / STREAM_R * STREAM_R;
-        if (h->rows_alloc < stream_rows) h->rows_alloc = stream_rows;
-        const int64_t clu_rows = (n + CLU_RC - 1) / CLU_RC * CLU_RC;
-        if (h->rows_alloc < clu_rows) h->rows_alloc = clu_rows;
         if (h->periodic) {
             if (h->K == 2) {
                 h->srow[0] = n - 4;
@@ -714,9 +542,7 @@ static int factor_impl(Band *h, const double *a, const double *b, const double *
             PB_CUDA_TRY(cudaFreeAsync(mfD, st));
             PB_CUDA_TRY(cudaFreeAsync(mbD, st));
         }
-        if ((rc = stream_build_tables(h, st))) return rc;
-        if ((rc = cluster_build_tables(h, st))) return rc;
-        if ((rc = twopass_build_tables(h, st))) return rc;
+        if ((rc = fused_build_tables(h, st))) return rc;
     } else {
         const int64_t M = h->batch;
         double *pcD = nullptr;
@@ -774,26 +600,12 @@ static int solve_impl(const Band *h, void *rhs, int layout, int64_t count, int64
     if (rc) return rc;
     sx.out_to(rhs);
     const bool al = (uintptr_t)sx.dev % 16 == 0 && (h->batch * es) % 16 == 0 && (count == 1 || (bstride * es) % 16 == 0);
-    // interleaved shared-LHS solver: the two-pass TMA streaming solve (default,
-    // fastest measured on B200 at the bench configuration), the
-    // TMA cluster kernel (PB_SOLVER=cluster), the register-tile cluster kernel
-    // (PB_SOLVER=tile) or the persistent streaming kernel (PB_SOLVER=stream)
-    const char *solver = getenv("PB_SOLVER");
-    const bool want_stream = (solver && !strcmp(solver, "stream")) || getenv("PB_STREAM");
-    const bool want_tile = solver && !strcmp(solver, "tile");
-    const bool want_clu = solver && !strcmp(solver, "cluster");
+    // interleaved shared-LHS solve: the fused streaming solve (fused_solve.cuh);
+    // the register-tile kernel serves the contiguous layout and unaligned buffers,
+    // one thread per system serves per-system LHS
     const bool inter = h->shared() && layout == PB_INTERLEAVED && al;
-    // (count > 1 stays off the two-pass path: batched launches faulted
-    // intermittently there under sustained back-to-back solves, tools/iso_stress.sh)
-    if (inter && !want_stream && !want_tile && !want_clu && h->tplan.ok && count == 1)
-        rc = h->dtype == PB_F64 ? launch_tp_f64(h, sx.dev, count, bstride, st)
-                                : launch_tp_f32(h, sx.dev, count, bstride, st);
-    else if (inter && want_stream && h->splan.ok)
-        rc = h->dtype == PB_F64 ? launch_stream_f64(h, sx.dev, count, bstride, st)
-                                : launch_stream_f32(h, sx.dev, count, bstride, st);
-    else if (inter && !want_tile && h->cplan.ok)
-        rc = h->dtype == PB_F64 ? launch_clu_f64(h, sx.dev, count, bstride, st)
-                                : launch_clu_f32(h, sx.dev, count, bstride, st);
+    if (inter && h->fplan.ok)
+        rc = launch_fused(h, sx.dev, count, bstride, st);
     else if (h->shared() && h->plan.C > 0)
         rc = h->dtype == PB_F64
                  ? (h->K == 2 ? launch_tile_f64_k2(h, sx.dev, layout, count, bstride, st)

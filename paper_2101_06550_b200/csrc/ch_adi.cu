@@ -398,14 +398,11 @@ static int adi_run(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nst
     A.k_bih = T(-(2.0 / 3.0) * dt * p->D * p->gamma / (dx * dx * dx * dx));
     A.k_lap = T((2.0 / 3.0) * p->D * dt / (dx * dx));
     A.w = (T *)s->work;
-    // y-sweep path: the fused band_core pass B (default) or, opt-in (PB_ADI_YSWEEP=tp), the
-    // two-pass solve over one batch of sims * n systems + combine: 3.95 vs 4.68 ms per cfg4
-    // step, but it faulted in ~1 of 10 runs of 23 steps (tools/adi_stress.sh) and stays
-    // opt-in until that is understood
-    const char *ys = getenv("PB_ADI_YSWEEP");
-    const bool ysweep_tp = h->tplan.ok && (ys && !strcmp(ys, "tp")) && (n * (int64_t)sizeof(T)) % 16 == 0 &&
-                           (uintptr_t)s->work % 16 == 0 && (uintptr_t)s->c_cur % 16 == 0 &&
-                           (uintptr_t)s->c_prev % 16 == 0;
+    // y-sweep: the fused streaming solve over ONE batch of sims * n interleaved systems
+    // (w in the permuted layout) + the C^{n+1} combine; the fused band_core pass B
+    // serves the rest (unaligned buffers)
+    const bool ysweep_tp = h->fplan.ok && (n * (int64_t)sizeof(T)) % 16 == 0 && (uintptr_t)s->work % 16 == 0 &&
+                           (uintptr_t)s->c_cur % 16 == 0 && (uintptr_t)s->c_prev % 16 == 0;
     A.wperm = ysweep_tp ? s->sims : 0;
     for (int64_t step = 0; step < nsteps; ++step) {
         A.cn = (const T *)s->c_cur;
@@ -415,7 +412,7 @@ static int adi_run(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nst
             // y-sweep = the batched interleaved solve (systems = columns i, one batch
             // per simulation) by the two-pass TMA solve, then the C^{n+1} combine
             // (w is in the permuted layout: one batch of sims * n systems)
-            if ((rc = launch_tp_m(h, A.w, s->sims * n, st))) return rc;
+            if ((rc = launch_fused(h, A.w, 1, 0, st, s->sims * n))) return rc;
             int dev = 0, nsm = 0;
             PB_CUDA_TRY(cudaGetDevice(&dev));
             PB_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -505,6 +502,29 @@ extern "C" int ch_dist_pass_a(int64_t rows, int64_t n, int dtype, const void *cn
     cudaStream_t st = (cudaStream_t)stream;
     return dtype == PB_F64 ? dist_pass_a<double>(rows, n, cn_ext, cm_ext, w, dt, p, st)
                            : dist_pass_a<float>(rows, n, cn_ext, cm_ext, w, dt, p, st);
+}
+
+// y-sweep of a rank's column block (configs[4]): L_y v = w along j for ncols
+// interleaved columns of length n, in place, with the cached cyclic L_y.
+extern "C" int ch_dist_ysweep(int64_t ncols, int64_t n, int dtype, void *cols, double dt, const pb_ch_params *p,
+                              void *stream)
+{
+    using namespace pb;
+    if (!p || !cols || ncols < 1 || n < 8) return set_error(PB_EINVAL, "bad args");
+    if (dtype != PB_F64 && dtype != PB_F32) return set_error(PB_EINVAL, "bad dtype");
+    if (!(dt > 0) || !(p->L > 0)) return set_error(PB_EINVAL, "dt and L must be positive");
+    if ((ncols * (int64_t)dtype_size(dtype)) % 16 || (uintptr_t)cols % 16)
+        return set_error(PB_EINVAL, "ch_dist_ysweep needs 16-byte aligned rows (ncols * sizeof(T) % 16 == 0)");
+    if (pb_device_ok() != PB_OK) return PB_ECUDA;
+    if (!is_device_ptr(cols)) return set_error(PB_EINVAL, "ch_dist_ysweep buffers must be device memory");
+    cudaStream_t st = (cudaStream_t)stream;
+    const double dx = p->L / (double)n;  // r1
+    const double sigma = (2.0 / 3.0) * p->D * p->gamma * dt / (dx * dx * dx * dx);
+    Band *h = nullptr;
+    int rc = adi_band(n, sigma, dtype, st, &h);
+    if (rc) return rc;
+    if (!h->fplan.ok) return set_error(PB_EUNSUPPORTED, "no streaming plan for n = %lld", (long long)n);
+    return launch_fused(h, cols, 1, 0, st, ncols);
 }
 
 extern "C" int ch_dist_pack(int64_t rows, int64_t n, int64_t parts, int dtype, const void *w, void *packed,

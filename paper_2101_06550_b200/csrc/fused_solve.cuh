@@ -1,0 +1,692 @@
+// fused_solve.cuh — the shared-LHS interleaved solve as ONE persistent kernel
+// (pent_solve / tri_solve / pent_solve_many / the ADI y-sweep).
+//
+// The thesis solves one system per thread over all N rows (P:1712-1724,
+// P:1729): at N = M = 8192 that is a dependent chain of 16 K rows per thread
+// and < 2 warps per SM.  Here every system is cut into chunks of Q = 64 rows
+// and one consumer warp owns one TILE = (chunk q, group g of 32 consecutive
+// systems): lane = system, so every tile row is one contiguous 256 B (fp64) /
+// 128 B (fp32) segment of the interleaved array and every
+// coefficient read is a warp-uniform shared-memory broadcast.
+//
+// Three kinds of work share one launch:
+//   P1(g, q)  forward sweep of the tile with zero inflow -> forward carry
+//             yF = (g_{r1-2}, g_{r1-1}); the chunk's back-substitution carry
+//             with zero inflow is a linear functional of g (zB = sum W_k g_k,
+//             W_k = rows r0, r0+1 of L^{-1}), accumulated on the fly.  Reads f
+//             from HBM once, writes 4 values per (system, chunk).
+//   scan(g)   when all P1 tiles of group g are done, a team of NSW scan warps
+//             composes the affine chunk maps (Mf_q, Mb_q, H_q) over q -> the
+//             true inflows (yin_q, zin_q) and, cyclic, Navon's / Sherman–
+//             Morrison's pair x_l.
+//   P2(g, q)  forward sweep from yin_q, back substitution from zin_q with the
+//             tile in registers, cyclic correction x - Z x_l (eq:solve), x
+//             stored in place.  Its f re-read hits the L2 that P1(g) filled:
+//             P2(g) is scheduled D groups after P1(g), D sized so the lag
+//             window of f fits in L2 -> HBM traffic = read f once + write x once.
+//
+// Work order.  Items are numbered in one global order: for s = 0, 1, ...:
+// the nq P1 tiles of group s, then the nq P2 tiles of group s - D.  CTAs CLAIM
+// items NC at a time from a global ticket (one per consumer warp), so every
+// claimed item precedes every unclaimed one: the earliest incomplete item
+// never waits on anything later (P1 waits on nothing; P2(g) waits only on the
+// scan of g, whose P1 tiles all precede it and whose scan team, claimed in
+// group order, waits only on those) -> no deadlock, whatever the residency.
+//
+// Per CTA: 1 producer warp (claims, flags, TMA), NC consumer warps, NSW scan
+// warps.  Ring of NS slots (NS a multiple of NC): local item j goes to warp
+// j % NC and slot j % NS, so every slot is owned by ONE consumer warp and a
+// parity wait can never alias an older phase.  A slot holds the tile (TMA
+// 3-D/2-D box), the chunk's coefficient rows (1-D bulk copy; L2-resident),
+// and for P2 the tile's inflows and x_l (1-D bulk copies, issued after the
+// producer has acquired the group's scan flag).
+//
+// Tables (built once per LHS by fs_tables_kernel, fp64 maths rounded to T):
+//   rec[r]  = (F0, F1, F2, Wa, Wb, 0)        per row (P1)
+//   coef[r] = band_core layout (F0 F1 F2 - B1 B2 Z1 Z2) (P2)
+//   ct[q]   = (Mf_q, Mb_q, H_q) row-major 2x2 each
+//   rsp[j]  = response of g on cyclic row srow[j] to its chunk's forward inflow
+#pragma once
+#include <cuda.h>
+
+#include "band_core.cuh"
+#include "common.cuh"
+
+namespace pb {
+namespace fs {
+
+constexpr int Q = 64;    // rows per chunk (tile height)
+constexpr int TW = 32;   // systems per tile (lanes)
+constexpr int REC = 6;   // P1 row record length
+constexpr int NC = 4;    // consumer warps (= items per claim)
+constexpr int NSW = 3;   // scan warps (1 + NC + NSW = 8 warps: the full 255-register budget)
+constexpr int NTHREADS = 32 * (NC + 1 + NSW);
+template <typename T>
+constexpr int sbatch() { return 8; }   // scan records per register batch
+
+template <typename T>
+struct Cfg {
+    static constexpr int TILE = Q * TW;             // elements
+    static constexpr int COEF = Q * COEF_STRIDE;    // >= Q * REC
+    static constexpr int INF = TW * 4;              // (yin0, yin1, zin0, zin1) per lane
+    static constexpr int XL = TW * 2;
+    static constexpr int SLOT = TILE + COEF + INF + XL;
+    static constexpr int NS = sizeof(T) == 8 ? 8 : 16;
+    static_assert(NS % NC == 0, "ring slots must be a multiple of the consumer warps");
+};
+
+template <typename T>
+struct Args {
+    const T *rec, *coef, *ct, *rsp;
+    const double *scal;
+    T *car;             // [q][sys][4]: P1 (yF, zB) -> scan (yin, zin)
+    T *spec;            // [sys][4] zero-inflow g on the cyclic rows
+    T *xl;              // [sys][2]
+    T *x;               // the right-hand sides, solved in place
+    int64_t bstride;    // elements between batches
+    unsigned *cnt;      // [G] P1 tiles done (reset by the scan team)
+    unsigned *flag;     // [G] == epoch once the group is scanned
+    unsigned *tick;     // [0] item claims, [1] scan claims, [2] CTAs done (reset by the last CTA)
+    unsigned epoch;
+    int64_t n, M, nsys; // rows, systems per batch, padded systems over all batches (= 32 G)
+    int64_t items, nclaims;
+    int64_t srow[4];
+    int nq, count, Gb, G, D;
+    int qspec;          // first chunk holding a cyclic row (cyclic only)
+    int flat;           // batches contiguous and n % Q == 0: 2-D maps, row = b * n + r
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void lds2(const double *p, double &a, double &b)
+{
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(su32(p)));
+}
+__device__ __forceinline__ void lds2(const float *p, float &a, float &b)
+{
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(a), "=f"(b) : "r"(su32(p)));
+}
+__device__ __forceinline__ void bar_init(uint64_t *b, int cnt)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t *b, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t *b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t *b, uint32_t parity)
+{
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "FS_WAIT:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra FS_WAIT;\n}" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void tma_load3(void *dst, const CUtensorMap *m, int c0, int c1, int c2, uint64_t *bar,
+                                          uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(su32(dst)),
+        "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load2(void *dst, const CUtensorMap *m, int c0, int c1, uint64_t *bar, uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(su32(dst)),
+        "l"(m), "r"(c0), "r"(c1), "r"(su32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     su32(dst)),
+                 "l"(src), "r"(bytes), "r"(su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p)
+{
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned *p)
+{
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned *p, unsigned v)
+{
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void scan_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * NSW) : "memory"); }
+__device__ __forceinline__ uint32_t up16(uint32_t b) { return (b + 15u) & ~15u; }
+
+// global item i -> (P2?, group, chunk); see the work order above
+struct Item {
+    int p2, g, q;
+};
+__device__ __forceinline__ Item decode(int64_t i, int nq, int G, int D)
+{
+    Item it;
+    const int64_t a = (int64_t)D * nq;                  // phase A: P1 of groups 0 .. D-1
+    const int64_t b = a + (int64_t)(G - D) * 2 * nq;    // phase B: (P1 of s, P2 of s - D), s = D .. G-1
+    if (i < a) {
+        it.p2 = 0;
+        it.g = (int)(i / nq);
+        it.q = (int)(i - (int64_t)it.g * nq);
+    } else if (i < b) {
+        const int64_t k = i - a, s = k / (2 * nq);
+        const int r = (int)(k - s * 2 * nq);
+        it.p2 = r >= nq;
+        it.g = (int)(it.p2 ? s : s + D);
+        it.q = it.p2 ? r - nq : r;
+    } else {                                            // phase C: P2 of groups G-D .. G-1
+        const int64_t k = i - b, s = k / nq;
+        it.p2 = 1;
+        it.g = (int)(G - D + s);
+        it.q = (int)(k - s * nq);
+    }
+    return it;
+}
+
+// ---------------------------------------------------------------- tile kernels (one warp)
+// P1: zero-inflow forward sweep, carry and back-substitution functional.
+// FULL: kmax == Q (no row guards); SPEC: the tile holds cyclic rows (ks[j] =
+// row srow[j] - r0 inside the tile, else -1)
+template <typename T, int K, bool SPEC, bool FULL>
+__device__ __forceinline__ void tile_carry(const T *d, const T *c, int kmax, int lane, const int (&ks)[4],
+                                           const Args<T> &A, int64_t sys, bool ok, int q)
+{
+    T y0 = T(0), y1 = T(0), a0 = T(0), a1 = T(0);
+#pragma unroll(FULL ? Q : 4)
+    for (int k = 0; k < (FULL ? Q : kmax); ++k) {
+        T f0, f1, f2, wa;
+        lds2(c + k * REC, f0, f1);
+        lds2(c + k * REC + 2, f2, wa);
+        const T wb = c[k * REC + 4];
+        T g = f0 * d[k * TW + lane] - f1 * y1;
+        if (K == 2) g -= f2 * y0;
+        y0 = y1;
+        y1 = g;
+        a0 += wa * g;
+        a1 += wb * g;
+        if (SPEC) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (ok && ks[j] == k) A.spec[sys * 4 + j] = g;
+        }
+    }
+    if (ok) {
+        T *o = A.car + ((int64_t)q * A.nsys + sys) * 4;
+        o[0] = y0;
+        o[1] = y1;
+        o[2] = a0;
+        o[3] = a1;
+    }
+}
+
+// P2: forward sweep from (y0, y1), back substitution from (z0, z1), cyclic
+// correction x - Z x_l, on the tile column in registers.  FULL: kmax == Q.
+template <typename T, int K, bool PER, bool FULL>
+__device__ __forceinline__ void tile_solve(T (&v)[Q], const T *c, int kmax, T y0, T y1, T z0, T z1, T xl0, T xl1)
+{
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+        if (FULL || k < kmax) {
+            T f0, f1;
+            lds2(c + k * COEF_STRIDE, f0, f1);
+            T g = f0 * v[k] - f1 * y1;
+            if (K == 2) g -= c[k * COEF_STRIDE + 2] * y0;
+            y0 = y1;
+            y1 = g;
+            v[k] = g;
+        }
+    }
+#pragma unroll
+    for (int k = Q - 1; k >= 0; --k) {
+        if (FULL || k < kmax) {
+            T b1, b2;
+            lds2(c + k * COEF_STRIDE + 4, b1, b2);
+            T xx = v[k] - b1 * z0;
+            if (K == 2) xx -= b2 * z1;
+            z1 = z0;
+            z0 = xx;
+            v[k] = xx;
+        }
+    }
+    if (PER) {
+        // cyclic correction x - Z x_l (Navon eq:solve / Sherman–Morrison)
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+            T z1v, z2v;
+            lds2(c + k * COEF_STRIDE + 6, z1v, z2v);
+            T o = v[k] - z1v * xl0;
+            if (K == 2) o -= z2v * xl1;
+            v[k] = o;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- scan of one group (NSW warps)
+template <typename T>
+__device__ __forceinline__ void mv(const T *m, T x0, T x1, T &r0, T &r1)
+{
+    r0 = m[0] * x0 + m[1] * x1;
+    r1 = m[2] * x0 + m[3] * x1;
+}
+template <typename T>
+__device__ __forceinline__ void mmul(const T *a, const T *b, T *r)   // r = a b (may alias)
+{
+    const T r0 = a[0] * b[0] + a[1] * b[2], r1 = a[0] * b[1] + a[1] * b[3];
+    const T r2 = a[2] * b[0] + a[3] * b[2], r3 = a[2] * b[1] + a[3] * b[3];
+    r[0] = r0, r[1] = r1, r[2] = r2, r[3] = r3;
+}
+template <typename T>
+__device__ __forceinline__ void ldm4(const T *p, T *m)
+{
+    m[0] = __ldg(p), m[1] = __ldg(p + 1), m[2] = __ldg(p + 2), m[3] = __ldg(p + 3);
+}
+template <typename T>
+__device__ __forceinline__ void ld_rec(const T *p, T *r)
+{
+    if (sizeof(T) == 8) {
+        const double2 u = __ldcg(reinterpret_cast<const double2 *>(p)), w = __ldcg(reinterpret_cast<const double2 *>(p + 2));
+        r[0] = (T)u.x, r[1] = (T)u.y, r[2] = (T)w.x, r[3] = (T)w.y;
+    } else {
+        const float4 u = __ldcg(reinterpret_cast<const float4 *>(p));
+        r[0] = (T)u.x, r[1] = (T)u.y, r[2] = (T)u.z, r[3] = (T)u.w;
+    }
+}
+template <typename T>
+__device__ __forceinline__ void st_rec(T *p, const T *r)
+{
+    if (sizeof(T) == 8) {
+        __stcg(reinterpret_cast<double2 *>(p), make_double2((double)r[0], (double)r[1]));
+        __stcg(reinterpret_cast<double2 *>(p + 2), make_double2((double)r[2], (double)r[3]));
+    } else {
+        __stcg(reinterpret_cast<float4 *>(p), make_float4((float)r[0], (float)r[1], (float)r[2], (float)r[3]));
+    }
+}
+
+template <typename T>
+struct ScanSmem {
+    T agg[NSW][TW][2];
+    T pm[NSW][4];
+    T gsp[4][TW];
+    int grp;
+};
+
+// The team's NSW warps split the group's chunks into NSW segments: fold each
+// segment (forward affine maps), combine the segment maps through shared
+// memory, walk the segment writing yin_q and c_q = zB_q + H_q yin_q; then the
+// same backward with Mb over c_q -> zin_q.  Records stay in place:
+// (yF, zB) -> (yin, zin).  Cyclic: warp 0 evaluates x_l.
+template <typename T, int K, bool PER>
+__device__ void scan_group(const Args<T> &A, ScanSmem<T> &S, int g, int sw, int lane)
+{
+    const int64_t sys = (int64_t)g * TW + lane;
+    const int nq = A.nq, cps = (nq + NSW - 1) / NSW;
+    const int qa = min(nq, sw * cps), qe = min(nq, qa + cps);
+    T *car = A.car + sys * 4;
+    const int64_t qstride = A.nsys * 4;
+    constexpr int SB = sbatch<T>();
+
+    // ---- forward fold of my segment: a = (Mf a + yF) over q, P = prod Mf
+    T P[4] = {T(1), T(0), T(0), T(1)}, a0 = T(0), a1 = T(0);
+    for (int q0 = qa; q0 < qe; q0 += SB) {
+        T R[SB][4];
+#pragma unroll
+        for (int i = 0; i < SB; ++i)
+            if (q0 + i < qe) ld_rec(car + (q0 + i) * qstride, R[i]);
+#pragma unroll
+        for (int i = 0; i < SB; ++i)
+            if (q0 + i < qe) {
+                T m[4], t0, t1;
+                ldm4(A.ct + (int64_t)(q0 + i) * 12, m);
+                mv(m, a0, a1, t0, t1);
+                a0 = t0 + R[i][0];
+                a1 = t1 + R[i][1];
+                mmul(m, P, P);
+            }
+    }
+    S.agg[sw][lane][0] = a0;
+    S.agg[sw][lane][1] = a1;
+    if (lane == 0)
+        for (int e = 0; e < 4; ++e) S.pm[sw][e] = P[e];
+    scan_bar();
+    T y0 = T(0), y1 = T(0);
+    for (int v = 0; v < sw; ++v) {
+        T t0, t1;
+        mv(S.pm[v], y0, y1, t0, t1);
+        y0 = t0 + S.agg[v][lane][0];
+        y1 = t1 + S.agg[v][lane][1];
+    }
+    // ---- forward walk: yin_q replaces yF_q, c_q = zB_q + H_q yin_q replaces zB_q
+    for (int q0 = qa; q0 < qe; q0 += SB) {
+        T R[SB][4];
+#pragma unroll
+        for (int i = 0; i < SB; ++i)
+            if (q0 + i < qe) ld_rec(car + (q0 + i) * qstride, R[i]);
+#pragma unroll
+        for (int i = 0; i < SB; ++i)
+            if (q0 + i < qe) {
+                const int q = q0 + i;
+                T m[4], h[4], t0, t1;
+                ldm4(A.ct + (int64_t)q * 12, m);
+                ldm4(A.ct + (int64_t)q * 12 + 8, h);
+                const T yf0 = R[i][0], yf1 = R[i][1];
+                mv(h, y0, y1, t0, t1);
+                R[i][0] = y0;
+                R[i][1] = y1;
+                R[i][2] += t0;
+                R[i][3] += t1;
+                if (PER && q >= A.qspec) {
+#pragma unroll
+                    for (int jx = 0; jx < 4; ++jx)
+                        if (A.srow[jx] >= 0 && A.srow[jx] / Q == q)
+                            S.gsp[jx][lane] = __ldcg(A.spec + sys * 4 + jx) + A.rsp[jx * 2] * y0 + A.rsp[jx * 2 + 1] * y1;
+                }
+                mv(m, y0, y1, t0, t1);
+                y0 = t0 + yf0;
+                y1 = t1 + yf1;
+                st_rec(car + q * qstride, R[i]);
+            }
+    }
+    // ---- backward fold of my segment (high to low): c = Mb c + c_q, Pb = prod Mb
+    T Pb[4] = {T(1), T(0), T(0), T(1)}, c0 = T(0), c1 = T(0);
+    for (int q1 = qe; q1 > qa; q1 -= SB) {
+        T R[SB][4];
+#pragma unroll
+        for (int i = 0; i < SB; ++i)
+            if (q1 - 1 - i >= qa) ld_rec(car + (q1 - 1 - i) * qstride, R[i]);
+#pragma unroll
+        for (int i = 0; i < SB; ++i)
+            if (q1 - 1 - i >= qa) {
+                T m[4], t0, t1;
+                ldm4(A.ct + (int64_t)(q1 - 1 - i) * 12 + 4, m);
+                mv(m, c0, c1, t0, t1);
+                c0 = t0 + R[i][2];
+                c1 = t1 + R[i][3];
+                mmul(m, Pb, Pb);
+            }
+    }
+    scan_bar();   // forward aggregates consumed
+    S.agg[sw][lane][0] = c0;
+    S.agg[sw][lane][1] = c1;
+    if (lane == 0)
+        for (int e = 0; e < 4; ++e) S.pm[sw][e] = Pb[e];
+    scan_bar();
+    T z0 = T(0), z1 = T(0);
+    for (int v = NSW - 1; v > sw; --v) {
+        T t0, t1;
+        mv(S.pm[v], z0, z1, t0, t1);
+        z0 = t0 + S.agg[v][lane][0];
+        z1 = t1 + S.agg[v][lane][1];
+    }
+    for (int q1 = qe; q1 > qa; q1 -= SB) {
+        T R[SB][4];
+#pragma unroll
+        for (int i = 0; i < SB; ++i)
+            if (q1 - 1 - i >= qa) ld_rec(car + (q1 - 1 - i) * qstride, R[i]);
+#pragma unroll
+        for (int i = 0; i < SB; ++i)
+            if (q1 - 1 - i >= qa) {
+                const int q = q1 - 1 - i;
+                T m[4], t0, t1;
+                ldm4(A.ct + (int64_t)q * 12 + 4, m);
+                const T cq0 = R[i][2], cq1 = R[i][3];
+                R[i][2] = z0;
+                R[i][3] = z1;
+                mv(m, z0, z1, t0, t1);
+                z0 = t0 + cq0;
+                z1 = t1 + cq1;
+                st_rec(car + q * qstride, R[i]);
+            }
+    }
+    if (PER && sw == 0) {
+        // (x_0, x_1) of the non-cyclic solution = warp 0's z after its walk
+        const T y1c = z0, y2c = z1;
+        T gv[4];
+#pragma unroll
+        for (int jx = 0; jx < 4; ++jx) gv[jx] = A.srow[jx] >= 0 ? S.gsp[jx][lane] : T(0);
+        const double *sc = A.scal;
+        T xl0, xl1;
+        if (K == 2) {
+            // Navon (eq:first_two)
+            const T ym1 = gv[1], ym2 = gv[0] - T(sc[10]) * gv[1];
+            const T q0 = gv[2] - (T(sc[4]) * y1c + T(sc[5]) * ym2 + T(sc[6]) * ym1);
+            const T q1 = gv[3] - (T(sc[7]) * y1c + T(sc[8]) * y2c + T(sc[9]) * ym1);
+            xl0 = T(sc[0]) * q0 + T(sc[1]) * q1;
+            xl1 = T(sc[2]) * q0 + T(sc[3]) * q1;
+        } else {
+            // Sherman–Morrison
+            xl0 = (y1c + T(sc[0]) * gv[0]) / T(sc[1]);
+            xl1 = T(0);
+        }
+        __stcg(A.xl + sys * 2 + 0, xl0);
+        __stcg(A.xl + sys * 2 + 1, xl1);
+    }
+}
+
+// ---------------------------------------------------------------- the kernel
+template <typename T>
+struct Smem {
+    T slot[Cfg<T>::NS][Cfg<T>::SLOT];
+    uint64_t full[Cfg<T>::NS], empty[Cfg<T>::NS];
+    int64_t item[Cfg<T>::NS];   // global item of the slot; -1 exit, -2 empty (past the end)
+    ScanSmem<T> scan;
+};
+
+template <typename T, int K, bool PER>
+__global__ void __launch_bounds__(NTHREADS, 1) fs_kernel(const __grid_constant__ CUtensorMap tmap, const Args<T> A)
+{
+    constexpr int NS = Cfg<T>::NS, TILE = Cfg<T>::TILE;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Smem<T> &sm = *reinterpret_cast<Smem<T> *>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NS; ++i) {
+            bar_init(&sm.full[i], 1);
+            bar_init(&sm.empty[i], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == NC) {
+        // ---------------- producer: claim NC items at a time, one per consumer warp
+        if (lane == 0) {
+            const uint64_t pol1 = policy_evict_last(), pol2 = policy_evict_first();
+            int64_t c = atomicAdd(A.tick, 1u);
+            for (int64_t k = 0;; ++k) {
+                const bool done = c >= A.nclaims;
+                const int64_t cn = done ? c : (int64_t)atomicAdd(A.tick, 1u);   // next claim, consumed one round later
+                Item it[NC];
+                unsigned fl[NC];
+#pragma unroll
+                for (int w = 0; w < NC; ++w) {
+                    const int64_t i = c * NC + w;
+                    it[w] = (!done && i < A.items) ? decode(i, A.nq, A.G, A.D) : Item{0, 0, 0};
+                    fl[w] = (!done && i < A.items && it[w].p2) ? ld_relaxed(A.flag + it[w].g) : A.epoch;
+                }
+#pragma unroll
+                for (int w = 0; w < NC; ++w) {
+                    const int64_t j = k * NC + w, i = c * NC + w;
+                    const int sl = (int)(j % NS);
+                    if (j >= NS) bar_wait(&sm.empty[sl], (uint32_t)(((j / NS) - 1) & 1));
+                    if (done || i >= A.items) {
+                        sm.item[sl] = done ? -1 : -2;
+                        bar_arrive(&sm.full[sl]);
+                        continue;
+                    }
+                    const Item id = it[w];
+                    if (id.p2) {
+                        // the group's scan must be complete before its inflows are copied
+                        if (fl[w] != A.epoch)
+                            while (ld_acquire(A.flag + id.g) != A.epoch) __nanosleep(64);
+                        fence_acquire();
+                        fence_proxy_global();
+                    }
+                    sm.item[sl] = i;
+                    const int b = id.g / A.Gb, gl = id.g - b * A.Gb;
+                    const int64_t r0 = (int64_t)id.q * Q;
+                    const int kmax = (int)min((int64_t)Q, A.n - r0);
+                    T *slot = sm.slot[sl];
+                    const uint32_t cb = up16((uint32_t)(kmax * (id.p2 ? COEF_STRIDE : REC) * sizeof(T)));
+                    uint32_t bytes = TILE * sizeof(T) + cb;
+                    if (id.p2) bytes += Cfg<T>::INF * sizeof(T) + (PER ? Cfg<T>::XL * sizeof(T) : 0);
+                    bar_expect_tx(&sm.full[sl], bytes);
+                    const uint64_t pol = id.p2 ? pol2 : pol1;
+                    if (A.flat)
+                        tma_load2(slot, &tmap, gl * TW, (int)((int64_t)b * A.n + r0), &sm.full[sl], pol);
+                    else
+                        tma_load3(slot, &tmap, gl * TW, (int)r0, b, &sm.full[sl], pol);
+                    bulk_load(slot + TILE, id.p2 ? A.coef + r0 * COEF_STRIDE : A.rec + r0 * REC, cb, &sm.full[sl]);
+                    if (id.p2) {
+                        bulk_load(slot + TILE + Cfg<T>::COEF, A.car + ((int64_t)id.q * A.nsys + (int64_t)id.g * TW) * 4,
+                                  Cfg<T>::INF * sizeof(T), &sm.full[sl]);
+                        if (PER)
+                            bulk_load(slot + TILE + Cfg<T>::COEF + Cfg<T>::INF, A.xl + (int64_t)id.g * TW * 2,
+                                      Cfg<T>::XL * sizeof(T), &sm.full[sl]);
+                    }
+                }
+                if (done) break;
+                c = cn;
+            }
+        }
+    } else if (warp < NC) {
+        // ---------------- consumers: local items j = warp, warp + NC, ... (slot j % NS, owned by this warp)
+        for (int64_t j = warp;; j += NC) {
+            const int sl = (int)(j % NS);
+            bar_wait(&sm.full[sl], (uint32_t)((j / NS) & 1));
+            const int64_t i = *(volatile int64_t *)&sm.item[sl];
+            if (i == -1) break;
+            if (i < 0) {
+                __syncwarp();
+                if (lane == 0) bar_arrive(&sm.empty[sl]);
+                continue;
+            }
+            const Item id = decode(i, A.nq, A.G, A.D);
+            const int b = id.g / A.Gb, gl = id.g - b * A.Gb;
+            const int64_t r0 = (int64_t)id.q * Q;
+            const int kmax = (int)min((int64_t)Q, A.n - r0);
+            const T *d = sm.slot[sl];
+            const T *c = d + TILE;
+            const int64_t s_in_batch = (int64_t)gl * TW + lane;
+            const bool ok = s_in_batch < A.M;
+            const int64_t sys = (int64_t)id.g * TW + lane;
+            if (!id.p2) {
+                if (PER && id.q >= A.qspec) {
+                    int ks[4];
+#pragma unroll
+                    for (int jx = 0; jx < 4; ++jx) {
+                        const int64_t rr = A.srow[jx] - r0;
+                        ks[jx] = (A.srow[jx] >= 0 && rr >= 0 && rr < Q) ? (int)rr : -1;
+                    }
+                    tile_carry<T, K, true, false>(d, c, kmax, lane, ks, A, sys, ok, id.q);
+                } else {
+                    const int ks[4] = {-1, -1, -1, -1};
+                    if (kmax == Q) tile_carry<T, K, false, true>(d, c, Q, lane, ks, A, sys, ok, id.q);
+                    else tile_carry<T, K, false, false>(d, c, kmax, lane, ks, A, sys, ok, id.q);
+                }
+                __syncwarp();
+                if (lane == 0) bar_arrive(&sm.empty[sl]);
+                // publish: this tile's records (and cyclic g values) -> the group's counter
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) atomicAdd(A.cnt + id.g, 1u);
+                continue;
+            }
+            // P2: the column, inflows and x_l into registers
+            T v[Q];
+#pragma unroll
+            for (int k = 0; k < Q; ++k) v[k] = d[k * TW + lane];
+            const T *inf = c + Cfg<T>::COEF;
+            T y0, y1, z0, z1, xl0 = T(0), xl1 = T(0);
+            lds2(inf + lane * 4, y0, y1);
+            lds2(inf + lane * 4 + 2, z0, z1);
+            if (PER) lds2(inf + Cfg<T>::INF + lane * 2, xl0, xl1);
+            if (kmax == Q) tile_solve<T, K, PER, true>(v, c, Q, y0, y1, z0, z1, xl0, xl1);
+            else tile_solve<T, K, PER, false>(v, c, kmax, y0, y1, z0, z1, xl0, xl1);
+            __syncwarp();
+            if (lane == 0) bar_arrive(&sm.empty[sl]);
+            if (PER && K == 2 && r0 + Q > A.n - 2) {
+                // Navon: the last two unknowns are x_l itself
+                const int k2 = (int)(A.n - 2 - r0);
+#pragma unroll
+                for (int k = 0; k < Q; ++k) {
+                    if (k == k2) v[k] = xl0;
+                    if (k == k2 + 1) v[k] = xl1;
+                }
+            }
+            if (ok) {
+                // x in place: every row of the tile is one contiguous 32-system segment
+                // (opaque stride: one running address instead of Q live ones)
+                int64_t Mo = A.M;
+                asm volatile("" : "+l"(Mo));
+                T *x = A.x + (int64_t)b * A.bstride + r0 * Mo + s_in_batch;
+#pragma unroll
+                for (int k = 0; k < Q; ++k) {
+                    if (kmax == Q || k < kmax) __stcs(x, v[k]);
+                    x += Mo;
+                }
+            }
+        }
+    } else {
+        // ---------------- scan team: groups claimed in order, each after its P1 tiles
+        const int sw = warp - NC - 1;
+        for (;;) {
+            if (sw == 0 && lane == 0) sm.scan.grp = (int)atomicAdd(A.tick + 1, 1u);
+            scan_bar();
+            const int g = sm.scan.grp;
+            if (g >= A.G) break;
+            while (ld_acquire(A.cnt + g) < (unsigned)A.nq) __nanosleep(128);
+            scan_group<T, K, PER>(A, sm.scan, g, sw, lane);
+            __threadfence();
+            fence_proxy_global();
+            scan_bar();   // all records / x_l of the group written (and sm.scan.grp consumed)
+            if (sw == 0 && lane == 0) {
+                A.cnt[g] = 0u;
+                st_release(A.flag + g, A.epoch);
+            }
+        }
+    }
+    // the last CTA out resets the tickets for the next launch (stream-ordered)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(A.tick + 2, 1u) == gridDim.x - 1) {
+            A.tick[0] = 0u;
+            A.tick[1] = 0u;
+            A.tick[2] = 0u;
+            __threadfence();
+        }
+    }
+}
+
+}  // namespace fs
+}  // namespace pb

@@ -1,6 +1,6 @@
 """Row-partitioned ADI Cahn–Hilliard step over P ranks (configs[4]: one n x n
 grid); orchestration only — every arithmetic step runs in
-libpentab.so (ch_dist_pass_a, ch_dist_pack, pent_solve, ch_dist_combine).
+libpentab.so (ch_dist_pass_a, ch_dist_pack, ch_dist_ysweep, ch_dist_combine).
 
 Rank r owns rows [r n/P, (r+1) n/P).  One step of Eq 3.1:
   1. halo exchange: 2 rows above / below of C^n and C^{n-1} (periodic across
@@ -8,7 +8,7 @@ Rank r owns rows [r n/P, (r+1) n/P).  One step of Eq 3.1:
   2. RHS + x-sweep on the rank's rows (ch_dist_pass_a) -> w;
   3. pack w by column block and all-to-all: rank r receives the n x n/P
      column block r of w (rows in order, columns interleaved = the systems);
-  4. y-sweep: pent_solve on that block (cyclic L_y, batch n/P, interleaved);
+  4. y-sweep: ch_dist_ysweep on that block (cyclic L_y, n/P systems, interleaved);
   5. all-to-all back: rank r receives v for its rows, block q = columns of q;
   6. C^{n+1} = 2 C^n - C^{n-1} + v (ch_dist_combine), levels rotate.
 The exchange is the only communication (2 all-to-all of one field + halo
@@ -38,23 +38,13 @@ class Params:
     def rows(self) -> int:
         return self.n // self.parts
 
-    @property
-    def sigma(self) -> float:
-        dx = self.L / self.n
-        return (2.0 / 3.0) * self.D * self.gamma * self.dt / dx ** 4
 
 
 class LibCompute:
     """The product backend: libpentab.so kernels on the rank's device."""
 
     def __init__(self, prm: Params, device, dtype):
-        import torch
         self.prm, self.device, self.dtype = prm, device, dtype
-        s = prm.sigma
-        n = prm.n
-        diag = [torch.full((n,), v, dtype=torch.float64, device=device) for v in (s, -4 * s, 1 + 6 * s, -4 * s, s)]
-        self.ly = pb.pent_factor(*diag, batch=prm.n // prm.parts, n=n, periodic=True,
-                                 dtype="f64" if dtype == torch.float64 else "f32")
 
     def pass_a(self, cn_ext, cm_ext, w):
         p = self.prm
@@ -65,7 +55,8 @@ class LibCompute:
         pb.ch_dist_pack(w, packed, rows=p.rows, n=p.n, parts=p.parts)
 
     def ysolve(self, cols):
-        self.ly.solve(cols)
+        p = self.prm
+        pb.ch_dist_ysweep(cols, ncols=p.rows, n=p.n, dt=p.dt, D=p.D, gamma=p.gamma, L=p.L)
 
     def combine(self, cn_ext, cm_ext, v_packed):
         p = self.prm
@@ -134,11 +125,16 @@ class TorchExchange:
         up, dn = (k - 1) % P, (k + 1) % P
         ops, recv = [], []
         for f, buf in enumerate((st.cn, st.cm)):
-            # tags keep the two directions apart when up == dn (P = 2)
+            # NCCL matches the k-th send to a peer with the k-th receive from it
+            # and ignores tags, so the posting order itself must pair up when
+            # up == dn (P = 2): every rank posts send(bottom rows -> dn) before
+            # send(top rows -> up), and recv(<- up) before recv(<- dn); the peer's
+            # first message is then its bottom rows = our upper halo.  Tags (gloo)
+            # agree with that pairing.
             t_up, t_dn = 1 + 2 * f, 2 + 2 * f
             top, bot = buf[2:4].contiguous(), buf[r:r + 2].contiguous()
             rt, rb = buf.new_empty((2, buf.shape[1])), buf.new_empty((2, buf.shape[1]))
-            ops += [dist.P2POp(dist.isend, top, up, self.group, t_up), dist.P2POp(dist.isend, bot, dn, self.group, t_dn),
+            ops += [dist.P2POp(dist.isend, bot, dn, self.group, t_dn), dist.P2POp(dist.isend, top, up, self.group, t_up),
                     dist.P2POp(dist.irecv, rt, up, self.group, t_dn), dist.P2POp(dist.irecv, rb, dn, self.group, t_up)]
             recv.append((buf, rt, rb))
         for req in dist.batch_isend_irecv(ops):

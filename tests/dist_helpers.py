@@ -27,7 +27,7 @@ def _lap_weights(dx):
 class OracleCompute:
     def __init__(self, prm):
         self.prm = prm
-        s = prm.sigma
+        s = (2.0 / 3.0) * prm.D * prm.gamma * prm.dt / (prm.L / prm.n) ** 4   # L_y
         self.diag = [np.full(prm.n, v) for v in (s, -4 * s, 1 + 6 * s, -4 * s, s)]
 
     def pass_a(self, cn_ext, cm_ext, w):

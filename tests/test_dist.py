@@ -78,3 +78,83 @@ def test_gloo_two_ranks_match_single_grid():
     prm, c0, c1 = _setup(n, world)
     ref, _ = oracle.ch_adi_steps(c1, c0, 2, dt=prm.dt, D=1.0, gamma=0.01, L=prm.L)
     assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) <= 1e-12
+
+
+class _FakeNccl:
+    """torch.distributed stand-in with NCCL's point-to-point matching: the k-th
+    send from a to b pairs with the k-th receive on b from a, tags ignored."""
+
+    import queue as _q
+    import threading as _t
+
+    def __init__(self, world):
+        self.world = world
+        self.chan = {(a, b): self._q.Queue() for a in range(world) for b in range(world)}
+        self.local = self._t.local()
+
+    def get_world_size(self, group=None):
+        return self.world
+
+    def get_rank(self, group=None):
+        return self.local.rank
+
+    def isend(self):  # markers only
+        pass
+
+    def irecv(self):
+        pass
+
+    class P2POp:
+        def __init__(self, op, tensor, peer, group=None, tag=0):
+            self.op, self.tensor, self.peer = op, tensor, peer
+
+    def batch_isend_irecv(self, ops):
+        me = self.local.rank
+        reqs = []
+        for o in ops:
+            if o.op == self.isend:
+                self.chan[(me, o.peer)].put(o.tensor.clone())
+        for o in ops:
+            if o.op == self.irecv:
+                reqs.append((o.tensor, self.chan[(o.peer, me)]))
+
+        class _Req:
+            def __init__(self, t, ch):
+                self.t, self.ch = t, ch
+
+            def wait(self):
+                self.t.copy_(self.ch.get(timeout=30))
+
+        return [_Req(t, ch) for t, ch in reqs]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_halo_posting_order_pairs_under_nccl_matching(world):
+    """The halo exchange must be correct when messages pair by posting order
+    (NCCL), not by tag: at P = 2 both neighbours are the same peer."""
+    import threading
+
+    n = 16
+    r = n // world if n % world == 0 else None
+    n = r * world if r else 12 * world
+    prm = dist.Params(n=n, parts=world, dt=0.01, L=1.0)
+    r = prm.rows
+    full = torch.arange(n * n, dtype=torch.float64).reshape(n, n)
+    fake = _FakeNccl(world)
+    ex = dist.TorchExchange()
+    ex.dist = fake
+    states = [dist.RankState(prm, k, full[k * r:(k + 1) * r], -full[k * r:(k + 1) * r], None) for k in range(world)]
+
+    def run(k):
+        fake.local.rank = k
+        ex.halo([states[k]])
+
+    th = [threading.Thread(target=run, args=(k,)) for k in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=60)
+    for k, st in enumerate(states):
+        rows = [(k * r + j) % n for j in range(-2, r + 2)]
+        assert torch.equal(st.cn, full[rows]), k
+        assert torch.equal(st.cm, -full[rows]), k

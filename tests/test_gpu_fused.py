@@ -1,7 +1,7 @@
-"""GPU parity of the two-pass streaming solve (twopass.cuh): the interleaved
+"""GPU parity of the fused streaming solve (fused_solve.cuh): the interleaved
 shared-LHS path of pent_solve / tri_solve with 64-row chunks, at sizes spanning
 one to hundreds of chunks, ragged last chunks (down to one row), system counts
-that are not multiples of the warp or CTA width, several L2 slabs, cyclic and
+that are not multiples of the warp or CTA width, batched launches, cyclic and
 non-cyclic, fp64 (<= 1e-12) and fp32 (<= 1e-5 against the fp64 oracle)."""
 import numpy as np
 import pytest
@@ -13,11 +13,6 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_2101_06550_b200 as pb  # noqa: E402
-
-
-@pytest.fixture(autouse=True)
-def _tp_path(monkeypatch):
-    monkeypatch.delenv("PB_SOLVER", raising=False)
 
 
 TOL = {"f64": 1e-12, "f32": 1e-5}
@@ -77,12 +72,10 @@ def test_tp_thesis_matrix(n, dtype):
     assert relerr(x.double().cpu().numpy(), ref) <= TOL[dtype]
 
 
-@pytest.mark.parametrize("slab_mb", ["0", "0.05", "1"])
-def test_tp_slabs_and_many(monkeypatch, slab_mb):
-    """count > 1 batches at a batch stride larger than batch*n, the systems split
-    into L2 slabs (PB_TP_SLAB_MB), repeated launches."""
-    monkeypatch.setenv("PB_TP_SLAB_MB", slab_mb)
-    n, m, cnt, pad = 1100, 300, 3, 17
+@pytest.mark.parametrize("n,m,cnt,pad", [(1100, 300, 3, 17), (512, 96, 5, 0), (64, 32, 7, 8)])
+def test_tp_many(n, m, cnt, pad):
+    """count > 1 batches (pent_solve_many) at a batch stride >= batch*n, repeated
+    launches; the padding between batches is untouched."""
     a, b, c, d, e = synth.dd_penta(n, 1, seed=11)
     f = synth.rhs_uniform(n, cnt * m, seed=12)
     ref = np.concatenate([oracle.penta_batch_solve(a, b, c, d, e, f[k * n * m:(k + 1) * n * m], n=n, m=m,
@@ -100,23 +93,10 @@ def test_tp_slabs_and_many(monkeypatch, slab_mb):
         assert bool((buf.view(cnt, bs)[:, n * m:] == 7.0).all())   # padding untouched
 
 
-def test_tp_matches_cluster_path(monkeypatch):
-    """The two-pass path and the TMA cluster path agree to rounding."""
-    n, m = 3000, 48
-    a, b, c, d, e = synth.dd_penta(n, 1, seed=21)
-    f = torch.from_numpy(synth.rhs_uniform(n, m, seed=22)).cuda()
-    h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in (a, b, c, d, e)], batch=m, n=n, periodic=True)
-    x1 = h.solve(f.clone())
-    monkeypatch.setenv("PB_SOLVER", "cluster")
-    x2 = h.solve(f.clone())
-    torch.cuda.synchronize()
-    assert float((x1 - x2).abs().max() / x2.abs().max()) <= 1e-13
-
-
 def test_tp_back_to_back_deterministic():
     """200 queued back-to-back solves (no host sync in between) equal the same
-    200 solves run one at a time with a sync after each: the pass-1 -> scan ->
-    pass-2 chain, its programmatic dependent launches and the per-handle scratch
+    200 solves run one at a time with a sync after each: the P1 -> scan -> P2
+    dependencies inside the kernel, the claim tickets and the per-stream scratch
     reuse are race-free."""
     n, m, reps = 2048, 1024, 200
     a, b, c, d, e = synth.dd_penta(n, 1, seed=31)
@@ -130,3 +110,46 @@ def test_tp_back_to_back_deterministic():
         h.solve(x2)
         torch.cuda.synchronize()
     assert torch.equal(x1, x2)
+
+
+def test_concurrent_streams_one_handle():
+    """Solves with ONE handle queued on two streams at once (per-stream scratch)
+    equal the same solves run one stream at a time."""
+    n, m, reps = 4096, 2048, 20
+    a, b, c, d, e = synth.dd_penta(n, 1, seed=41)
+    h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in (a, b, c, d, e)], batch=m, n=n, periodic=True)
+    f1 = torch.from_numpy(synth.rhs_uniform(n, m, seed=42)).cuda()
+    f2 = torch.from_numpy(synth.rhs_uniform(n, m, seed=43)).cuda()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    x1, x2 = f1.clone(), f2.clone()
+    torch.cuda.synchronize()
+    for _ in range(reps):
+        h.solve(x1, stream=s1)
+        h.solve(x2, stream=s2)
+    torch.cuda.synchronize()
+    y1, y2 = f1.clone(), f2.clone()
+    for _ in range(reps):
+        h.solve(y1)
+    for _ in range(reps):
+        h.solve(y2)
+    torch.cuda.synchronize()
+    assert torch.equal(x1, y1) and torch.equal(x2, y2)
+
+
+def test_shape_changes_reuse_scratch():
+    """One handle, one stream, alternating batch shapes (the scratch's counters move
+    with the shape): every solve matches the oracle."""
+    n = 700
+    a, b, c, d, e = synth.dd_penta(n, 1, seed=51)
+    h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in (a, b, c, d, e)], batch=96, n=n, periodic=True)
+    for cnt in (3, 1, 5, 1, 2):
+        f = synth.rhs_uniform(n, cnt * 96, seed=cnt)
+        ref = np.concatenate([oracle.penta_batch_solve(a, b, c, d, e, f[k * n * 96:(k + 1) * n * 96], n=n, m=96,
+                                                       periodic=True) for k in range(cnt)])
+        x = torch.from_numpy(f).cuda()
+        if cnt == 1:
+            h.solve(x)
+        else:
+            h.solve_many(x, cnt, n * 96)
+        torch.cuda.synchronize()
+        assert relerr(x.cpu().numpy(), ref) <= 1e-12
