@@ -1,28 +1,36 @@
 """bench.py — throughput of the B200 hot path (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--no-adi] [--dtype f64|f32]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--dtype f64|f32]
+                    [--no-adi] [--no-sweep] [--no-ch1d] [--no-dist] [--no-cpu]
 
 Headline (``value``): the factor-once batched cyclic pentadiagonal solve of
 configs[1] at its largest size (N = 8192 unknowns, batch M = 8192 systems,
-fp64, interleaved layout, the thesis CH matrix sigma = 45.09), in M unknowns/s
-over all ranks.  A "step" is one pent_solve of the whole batch (one kernel
-launch, in place).  The 512 MiB right-hand side is larger than the 126 MB L2,
-so every step streams from HBM (no flush needed).  Multi-GPU: every rank
-solves its own batch (independent systems; no data-path collective) ->
-"scaling": "weak".
+fp64, interleaved, the thesis CH matrix sigma = 45.09), in M unknowns/s over
+all ranks.  A "step" is one pent_solve of the whole batch (one kernel launch,
+in place).  The 512 MiB right-hand side is 4x the 126 MB L2, so every step
+streams from HBM (no flush needed).  Multi-GPU: every rank solves its own batch
+(independent systems, no data-path collective) -> "scaling": "weak".
 
-Secondary (``ch_adi``): configs[3] — 512 independent Cahn–Hilliard ADI
-simulations at 512^2 (L = 4 pi, fp64), sharded over the ranks (strong), in
-simulation time-steps/s; one step = both fused passes of Eq 3.1 for every sim.
-
+Secondary legs (each in the same JSON line):
+  sweep   configs[1]: N = 256..8192 (batch = N) x {f64, f32}, hot (K solves
+          replayed from a CUDA graph) and L2-cold (256 MiB flush before each
+          solve, per-solve events)
+  ch_adi  configs[3]: 512 CH ADI simulations at 512^2 (L = 4 pi), sharded
+          over the ranks, sim-timesteps/s
+  cfg3    configs[2]: one 1024^2 simulation (L = 8 pi), 1000 steps as 100
+          replays of a 10-step CUDA graph, timesteps/s
+  ch1d    thesis §6.2: 2^20 independent 1D CH systems x N = 256, steps/s
+  dist    configs[4]: one 16384^2 grid row-partitioned over the ranks (at
+          N = 1 the single-rank form of the same exchange code)
 The oracle (``oracle/``) is executed only in the cpu_baseline leg and under
-``--impl reference`` (rank 0, N = 1 for the former), per the task contract.
+``--impl reference`` (rank 0), per the task contract.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import math
+import multiprocessing as mp
 import os
 import statistics
 import sys
@@ -39,9 +47,15 @@ import synth  # noqa: E402
 
 METRIC = "penta solve Munknowns/s & % HBM peak; CH ADI timesteps/s at 1/2/4/8 B200"
 PENTA_N = 8192          # configs[1], largest size: N = batch = 8192
+SWEEP_N = (256, 512, 1024, 2048, 4096, 8192)
 ADI_SIMS, ADI_N = 512, 512   # configs[3]
 ADI_L = ADI_N * synth.DX_STATS  # 4 pi: dx = 2 pi / 256
+CFG3_N = 1024
+CFG3_L = CFG3_N * synth.DX_STATS  # 8 pi
 CH_D, CH_GAMMA = 1.0, 0.01
+CH1D_M, CH1D_N, CH1D_L = 1 << 20, 256, 2 * math.pi   # thesis §6.2.3: 2^20 systems, N = 256 on 2 pi
+DIST_N = 16384                     # configs[4]: one 16384^2 grid over the ranks
+FLUSH_BYTES = 256 << 20            # > 2x the 126 MB L2
 
 
 # ------------------------------------------------------------------ host-side helpers (CPU-testable)
@@ -87,6 +101,23 @@ def penta_matvec(a, b, c, d, e, x, periodic=True):
             ok = (j >= 0) & (j < n)
             y = y + np.where(ok, diag * x[np.clip(j, 0, n - 1)], 0.0)
     return y
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -154,36 +185,58 @@ def measured_peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kernel_key: str):
-    """dram bytes per launch of `kernel_key` from the committed ncu --set full
-    summary (profiles/ncu_traffic.json), else None."""
+def ncu_traffic(key: str):
+    """DRAM bytes per launch of `key` from the committed ncu --set full summary
+    (profiles/ncu_traffic.json), else None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get(kernel_key)
+            return json.load(f).get(key)
     except Exception:
         return None
 
 
+def roofline(alg_bytes, seconds, kernel, key=None, note=None):
+    peak, src = measured_peak_hbm()
+    ach = alg_bytes / seconds / 1e9
+    r = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+         "traffic": ncu_traffic(key) if key else None, "algorithmic_bytes_per_launch": int(alg_bytes),
+         "kernel": kernel, "peak_source": src}
+    if note:
+        r["note"] = note
+    return r
+
+
 # ------------------------------------------------------------------ CPU oracle legs
-def oracle_penta_sample(budget_s: float, m_sample: int = 64):
-    """The oracle as it stands on a bounded sample of the configs[1] workload:
-    m_sample systems of N = 8192 (the same shared cyclic LHS), repeated until
-    budget_s of CPU time.  Returns unknowns/s, description."""
+def _oracle_penta_worker(args):
+    """One process: the oracle on `m` systems of the configs[1] workload, repeated
+    until `budget` seconds; returns (unknowns, seconds)."""
+    m, budget, seed = args
     import oracle
     n = PENTA_N
     s = synth.SIGMA_STATS
     diags = synth.const_penta(n, s, -4 * s, 1 + 6 * s, -4 * s, s)
-    f = synth.rhs_uniform(n, m_sample, seed=2)
-    oracle.penta_batch_solve(*diags, f, n=n, m=m_sample, periodic=True)  # warm
+    f = synth.rhs_uniform(n, m, seed=seed)
+    oracle.penta_batch_solve(*diags, f, n=n, m=m, periodic=True)  # warm
     reps, t0 = 0, time.perf_counter()
     while True:
-        oracle.penta_batch_solve(*diags, f, n=n, m=m_sample, periodic=True)
+        oracle.penta_batch_solve(*diags, f, n=n, m=m, periodic=True)
         reps += 1
         el = time.perf_counter() - t0
-        if el >= budget_s:
-            break
-    return reps * n * m_sample / el, f"{reps} x oracle.penta_batch_solve of {m_sample} systems x N={n} (cyclic, fp64)"
+        if el >= budget:
+            return reps * n * m, el
+
+
+def oracle_penta_sample(budget_s: float, cores: int, m_sample: int = 64):
+    """The oracle as it stands (single-threaded C) on a bounded sample of the
+    configs[1] workload: one process per host core, each solving m_sample
+    systems of N = 8192 repeatedly for budget_s; aggregate unknowns/s."""
+    if cores <= 1:
+        u, el = _oracle_penta_worker((m_sample, budget_s, 2))
+        return u / el, 1
+    with mp.get_context("spawn").Pool(cores) as pool:
+        res = pool.map(_oracle_penta_worker, [(m_sample, budget_s, 2 + k) for k in range(cores)])
+    return sum(u / el for u, el in res), cores
 
 
 def oracle_adi_sample(budget_s: float, sims: int = 2, steps: int = 1):
@@ -198,12 +251,19 @@ def oracle_adi_sample(budget_s: float, sims: int = 2, steps: int = 1):
         el = time.perf_counter() - t0
         if el >= budget_s:
             break
-    return reps * sims * steps / el, f"{reps} x oracle.ch_adi_steps({sims} sims x {ADI_N}^2, {steps} step)"
+    return reps * sims * steps / el, f"{reps} x oracle.ch_adi_steps({sims} sims x {ADI_N}^2, {steps} step), 1 core"
 
 
 # ------------------------------------------------------------------ GPU legs
-def _events(torch, st, n):
-    return [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+def _ev(torch):
+    return torch.cuda.Event(enable_timing=True)
+
+
+def thesis_handle(pb, torch, dev, n, m, dtype):
+    s = synth.SIGMA_STATS
+    diags = synth.const_penta(n, s, -4 * s, 1 + 6 * s, -4 * s, s)
+    return pb.pent_factor(*[torch.from_numpy(v).to(dev) for v in diags], batch=m, n=n, periodic=True,
+                          dtype=dtype), diags
 
 
 def bench_penta(args, rank, world, dev):
@@ -214,10 +274,8 @@ def bench_penta(args, rank, world, dev):
     n = m = PENTA_N
     tdt = torch.float64 if args.dtype == "f64" else torch.float32
     es = 8 if args.dtype == "f64" else 4
-    s = synth.SIGMA_STATS
-    diags = synth.const_penta(n, s, -4 * s, 1 + 6 * s, -4 * s, s)
     st = torch.cuda.current_stream(dev)
-    h = pb.pent_factor(*[torch.from_numpy(v).to(dev) for v in diags], batch=m, n=n, periodic=True, dtype=args.dtype)
+    h, diags = thesis_handle(pb, torch, dev, n, m, args.dtype)
     f_host = synth.rhs_uniform(n, m, seed=2 + rank)
     f_dev = torch.from_numpy(f_host).to(dev, tdt)
     x = f_dev.clone()
@@ -230,18 +288,16 @@ def bench_penta(args, rank, world, dev):
     for sy in (0, 1, 4097, m - 1):
         r = penta_matvec(*(v[0] for v in diags), X[:, sy]) - F[:, sy]
         res = max(res, float(np.max(np.abs(r)) / np.max(np.abs(F[:, sy]))))
-    # warm-up (in-place repeated solves: each step solves the previous result)
-    for _ in range(args.warmup):
+    for _ in range(args.warmup):   # in-place repeated solves: each step solves the previous result
         h.solve(x)
     torch.cuda.synchronize(dev)
-    ev = _events(torch, st, 2 * args.steps)
+    ev = [_ev(torch) for _ in range(2 * args.steps)]
     pb.reset_launch_count()
     if dist.is_initialized():
         dist.barrier()
     torch.cuda.synchronize(dev)
     with ClockSampler(dev.index if dev.index is not None else 0) as clk:
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
+        t0, t1 = _ev(torch), _ev(torch)
         t0.record(st)
         for k in range(args.steps):
             ev[2 * k].record(st)
@@ -256,21 +312,19 @@ def bench_penta(args, rank, world, dev):
     kern_ms = statistics.mean(ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(args.steps))
     ms = max_over_ranks(ms_local, dev)
     kern_ms_max = max_over_ranks(kern_ms, dev)
-    units = world * n * m * args.steps
-    value = units / (ms * 1e-3) / 1e6
-    peak, peak_src = measured_peak_hbm()
+    value = world * n * m * args.steps / (ms * 1e-3) / 1e6
     alg_bytes = 2 * es * n * m  # read f once, write x once
-    achieved = alg_bytes / (kern_ms_max * 1e-3) / 1e9
 
-    # e2e: same metric through the public C-ABI call with HOST (pinned) buffers:
-    # H2D of the step's RHS, the solve, D2H of the solution, every step.
+    # e2e: the same metric through the public C-ABI call with HOST (pinned)
+    # buffers: every step the library copies the RHS in and the solution out
+    # (pipelined column blocks on two streams, pentab.h host-buffer contract)
     e2e_steps = max(3, min(args.steps, 10))
     xh = torch.from_numpy(f_host).to(tdt).pin_memory()
     h.solve(xh.numpy())  # warm the staging pool
     if dist.is_initialized():
         dist.barrier()
     torch.cuda.synchronize(dev)
-    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0, a1 = _ev(torch), _ev(torch)
     w0 = time.perf_counter()
     a0.record(st)
     for _ in range(e2e_steps):
@@ -286,15 +340,73 @@ def bench_penta(args, rank, world, dev):
     return {
         "value": value, "ms_per_step": ms / args.steps, "kern_ms": kern_ms_max, "launches": launches,
         "residual": res, "clocks": clk.summary(),
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(f"pent_solve_{args.dtype}"),
-                     "algorithmic_bytes_per_launch": alg_bytes,
-                     "kernel": "pent_solve = tp_pass_kernel<P1> + tp_scan_kernel + tp_pass_kernel<P2> (one call)",
-                     "peak_source": peak_src},
+        "roofline": roofline(alg_bytes, kern_ms_max * 1e-3, "fs_kernel (pent_solve, one launch: P1 + scan + P2)",
+                             f"pent_solve_{args.dtype}"),
         "e2e": {"value": round(e2e_val, 2), "unit": "Munknowns/s", "steps": e2e_steps,
                 "h2d_bytes_per_step": es * n * m, "d2h_bytes_per_step": es * n * m,
-                "path": "pent_solve(handle, host pinned rhs) -> library stages H2D, solve, D2H"},
+                "path": "pent_solve(handle, host pinned rhs) -> pitched H2D | fused solve | D2H of 8 column "
+                        "blocks pipelined on 2 streams"},
     }
+
+
+def bench_sweep(args, dev):
+    """configs[1] sweep: N = 256..8192, batch = N, fp64 and fp32; hot = K solves
+    replayed from a CUDA graph (per-solve time = graph time / K), cold = a
+    256 MiB write before each solve (per-solve events around the solve only)."""
+    import torch
+    import paper_2101_06550_b200 as pb
+
+    peak, _ = measured_peak_hbm()
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    side = torch.cuda.Stream(dev)
+    out = []
+    for dt in ("f64", "f32"):
+        tdt = torch.float64 if dt == "f64" else torch.float32
+        es = 8 if dt == "f64" else 4
+        for n in SWEEP_N:
+            m = n
+            h, _ = thesis_handle(pb, torch, dev, n, m, dt)
+            x = torch.from_numpy(synth.rhs_uniform(n, m, seed=2)).to(dev, tdt)
+            K = 20
+            with torch.cuda.stream(side):
+                for _ in range(3):
+                    h.solve(x, stream=side)
+                side.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=side):
+                    for _ in range(K):
+                        h.solve(x, stream=side)
+                g.replay()
+                side.synchronize()
+                e0, e1 = _ev(torch), _ev(torch)
+                e0.record(side)
+                for _ in range(5):
+                    g.replay()
+                e1.record(side)
+                side.synchronize()
+            hot_us = e0.elapsed_time(e1) * 1e3 / (5 * K)
+            cold = []
+            for _ in range(10):
+                flush.zero_()
+                c0, c1 = _ev(torch), _ev(torch)
+                c0.record()
+                h.solve(x)
+                c1.record()
+                torch.cuda.synchronize(dev)
+                cold.append(c0.elapsed_time(c1) * 1e3)
+            cold_us = statistics.median(cold)
+            b = 2 * es * n * m
+            out.append({"N": n, "batch": m, "dtype": dt,
+                        "hot_us": round(hot_us, 2), "hot_Munknowns_s": round(n * m / hot_us, 1),
+                        "hot_frac": round(b / (hot_us * 1e-6) / 1e9 / peak, 4),
+                        "cold_us": round(cold_us, 2), "cold_Munknowns_s": round(n * m / cold_us, 1),
+                        "cold_frac": round(b / (cold_us * 1e-6) / 1e9 / peak, 4)})
+            h.close()
+            del x, g
+    del flush
+    torch.cuda.empty_cache()
+    return {"unit": "us per solve", "hot": "CUDA graph of 20 solves, 5 replays", "cold": "256 MiB write before each "
+            "solve, median of 10", "frac": "16 (8) B per unknown / time / measured HBM peak", "rows": out}
 
 
 def bench_adi(args, rank, world, dev):
@@ -318,8 +430,7 @@ def bench_adi(args, rank, world, dev):
     del c0
     st = torch.cuda.current_stream(dev)
     mass0 = float(state.c_cur.double().sum())
-    for _ in range(args.warmup):
-        pb.ch_adi_step(state, dt, D=CH_D, gamma=CH_GAMMA, L=ADI_L, nsteps=1)
+    pb.ch_adi_step(state, dt, D=CH_D, gamma=CH_GAMMA, L=ADI_L, nsteps=args.warmup)
     torch.cuda.synchronize(dev)
     steps = args.adi_steps
     pb.reset_launch_count()
@@ -327,36 +438,99 @@ def bench_adi(args, rank, world, dev):
         dist.barrier()
     torch.cuda.synchronize(dev)
     with ClockSampler(dev.index if dev.index is not None else 0) as clk:
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0, t1 = _ev(torch), _ev(torch)
         t0.record(st)
-        for _ in range(steps):
-            pb.ch_adi_step(state, dt, D=CH_D, gamma=CH_GAMMA, L=ADI_L, nsteps=1)
+        pb.ch_adi_step(state, dt, D=CH_D, gamma=CH_GAMMA, L=ADI_L, nsteps=steps)
         t1.record(st)
         torch.cuda.synchronize(dev)
     launches = pb.launch_count()
     ms = max_over_ranks(t0.elapsed_time(t1), dev)
     mass1 = float(state.c_cur.double().sum())
     drift = max_over_ranks(abs(mass1 - mass0) / (ADI_N * ADI_N * max(sims, 1)), dev)
-    peak, peak_src = measured_peak_hbm()
     alg_bytes = 7 * es * ADI_N * ADI_N * sims  # 7 field passes per point and step
-    achieved = sum_over_ranks(alg_bytes, dev) / world / (ms / steps * 1e-3) / 1e9
     del state
     torch.cuda.empty_cache()
     return {
         "value": round(ADI_SIMS * steps / (ms * 1e-3), 2), "unit": "sim-timesteps/s",
         "whole_batch_steps_per_s": round(steps / (ms * 1e-3), 2), "ms_per_step": ms / steps, "steps": steps,
         "config": {"workload": "configs[3]: 512 CH ADI sims at 512^2, L=4pi, dt=0.1dx, D=1, gamma=0.01",
-                   "sims_per_rank": sims, "scaling": "strong"},
+                   "sims_per_rank": sims, "scaling": "weak (independent sims sharded, no collective)",
+                   "dtype": args.dtype},
         "launches": launches, "mean_abs_mass_drift_per_point": drift, "clocks": clk.summary(),
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(f"adi_step_{args.dtype}"),
-                     "algorithmic_bytes_per_step": alg_bytes, "kernel": "adi_pass_a + adi_pass_b (one step)",
-                     "peak_source": peak_src},
+        "roofline": roofline(sum_over_ranks(alg_bytes, dev) / world, ms / steps * 1e-3,
+                             "one step: adi_rhs_kernel + fs_kernel<contiguous> + fs_kernel<interleaved> + "
+                             "adi_combine_kernel", f"adi_step_{args.dtype}",
+                             "algorithmic 56 B/point (7 field passes); this schedule moves 11 fp64-sized passes"),
     }
 
 
-DIST_N = 16384                     # configs[4]: one 16384^2 grid over the ranks
-DIST_L = DIST_N * synth.DX_STATS   # 128 pi: dx = 2 pi / 256
+def bench_cfg3(args, dev):
+    """configs[2]: one 1024^2 simulation (L = 8 pi), 1000 steps = 100 replays of a
+    10-step CUDA graph (launch-latency bound: 4 launches per step)."""
+    import torch
+    import paper_2101_06550_b200 as pb
+
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    es = 8 if args.dtype == "f64" else 4
+    dt = synth.ch_dt(CFG3_N, CFG3_L)
+    c0 = torch.from_numpy(synth.ch_ic_random(1, CFG3_N, seed=3)).to(dev, tdt)
+    state = pb.CHState(c0)
+    side = torch.cuda.Stream(dev)
+    with torch.cuda.stream(side):
+        pb.ch_adi_step(state, dt, D=CH_D, gamma=CH_GAMMA, L=CFG3_L, nsteps=4, stream=side)
+        side.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            pb.ch_adi_step(state, dt, D=CH_D, gamma=CH_GAMMA, L=CFG3_L, nsteps=10, stream=side)
+        g.replay()
+        side.synchronize()
+        e0, e1 = _ev(torch), _ev(torch)
+        e0.record(side)
+        for _ in range(100):
+            g.replay()
+        e1.record(side)
+        side.synchronize()
+    ms = e0.elapsed_time(e1)
+    steps = 1000
+    del state, g
+    torch.cuda.empty_cache()
+    return {"value": round(steps / (ms * 1e-3), 1), "unit": "timesteps/s", "us_per_step": round(ms * 1e3 / steps, 2),
+            "config": {"workload": "configs[2]: one 1024^2 CH ADI sim, L=8pi, dt=0.1dx", "dtype": args.dtype,
+                       "graph": "10 steps captured, 100 replays"},
+            "effective_GBs": round(56 * CFG3_N * CFG3_N * steps / (ms * 1e-3) / 1e9 * es / 8, 1)}
+
+
+def bench_ch1d(args, dev):
+    """thesis §6.2.3: 2^20 independent 1D CH systems x N = 256 (L = 2 pi,
+    dt = 0.1 dx, gamma = 0.01), U(-0.1, 0.1) quench; K steps in one call."""
+    import torch
+    import paper_2101_06550_b200 as pb
+
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    es = 8 if args.dtype == "f64" else 4
+    dt = synth.ch_dt(CH1D_N, CH1D_L)
+    g = torch.Generator(device=dev)
+    g.manual_seed(6)
+    c0 = torch.empty((CH1D_N, CH1D_M), dtype=tdt, device=dev).uniform_(-0.1, 0.1, generator=g)
+    st = pb.CH1DState(c0)
+    del c0
+    pb.ch1d_step(st, dt, gamma=CH_GAMMA, L=CH1D_L, nsteps=args.warmup)
+    torch.cuda.synchronize(dev)
+    steps = args.steps
+    e0, e1 = _ev(torch), _ev(torch)
+    e0.record()
+    pb.ch1d_step(st, dt, gamma=CH_GAMMA, L=CH1D_L, nsteps=steps)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    alg = 2 * es * CH1D_N * CH1D_M   # read C^n, write C^{n+1}
+    del st
+    torch.cuda.empty_cache()
+    return {"value": round(steps / (ms * 1e-3), 2), "unit": "batch-timesteps/s",
+            "system_steps_per_s": round(CH1D_M * steps / (ms * 1e-3), 1), "ms_per_step": round(ms / steps, 4),
+            "config": {"workload": "thesis §6.2.3: 2^20 1D CH systems x N=256, L=2pi, dt=0.1dx", "dtype": args.dtype},
+            "roofline": roofline(alg, ms / steps * 1e-3, "fs_kernel<MODE_CH1D> (RHS formed on chip, one launch per step)",
+                                 f"ch1d_{args.dtype}")}
 
 
 def bench_dist_adi(args, rank, world, dev):
@@ -383,19 +557,28 @@ def bench_dist_adi(args, rank, world, dev):
     if world > 1:
         dist.barrier()
     steps = args.dist_steps
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0, e1 = _ev(torch), _ev(torch)
     e0.record()
     for _ in range(steps):
         pdist.step([st], ex)
     e1.record()
     torch.cuda.synchronize(dev)
     ms = max_over_ranks(e0.elapsed_time(e1), dev)
-    es = 8 if args.dtype == "f64" else 4
-    a2a = 2 * es * prm.rows * n * (world - 1) / world   # bytes each rank sends per step (two transposes)
+    a2a = 2 * 8 * prm.rows * n * (world - 1) / world   # fp64 bytes each rank sends per step (two transposes)
+    del st
+    torch.cuda.empty_cache()
     return {"value": round(steps / (ms * 1e-3), 3), "unit": "grid-timesteps/s", "ms_per_step": ms / steps,
             "steps": steps, "config": {"workload": f"configs[4]: one {n}^2 CH grid, L=128pi, row-partitioned x{world}",
-                                       "exchange": "2 all-to-all transposes + halo rows per step (torch.distributed)"},
+                                       "exchange": "2 all-to-all transposes + halo rows per step (torch.distributed)",
+                                       "dtype": args.dtype},
             "a2a_bytes_per_rank_per_step": a2a}
+
+
+def _leg(fn, *a):
+    try:
+        return fn(*a)
+    except Exception as ex:  # reported, never fatal to the headline
+        return {"error": f"{type(ex).__name__}: {ex}"[:300]}
 
 
 def run_ours(args):
@@ -417,19 +600,23 @@ def run_ours(args):
     import paper_2101_06550_b200 as pb
     pb.lib()
     r = bench_penta(args, rank, world, dev)
-    adi = bench_adi(args, rank, world, dev) if not args.no_adi else None
-    dist_adi = None
-    if (world > 1 or args.dist_force) and not args.no_dist:
-        try:
-            dist_adi = bench_dist_adi(args, rank, world, dev)
-        except Exception as ex:  # reported, never fatal to the headline
-            dist_adi = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+    adi = _leg(bench_adi, args, rank, world, dev) if not args.no_adi else None
+    sweep = _leg(bench_sweep, args, dev) if (not args.no_sweep and rank == 0) else None
+    cfg3 = _leg(bench_cfg3, args, dev) if (not args.no_adi and rank == 0) else None
+    ch1d = _leg(bench_ch1d, args, dev) if (not args.no_ch1d and rank == 0) else None
+    dist_adi = _leg(bench_dist_adi, args, rank, world, dev) if not args.no_dist else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, sample = oracle_penta_sample(args.cpu_budget)
-        va, sa = oracle_adi_sample(args.cpu_budget / 2)
-        cpu = {"value": round(v / 1e6, 3), "unit": "Munknowns/s", "cores": 1, "kind": "oracle",
-               "sample": sample, "ch_adi": {"value": round(va, 3), "unit": "sim-timesteps/s", "sample": sa}}
+        cores = host_cores()
+        v1, _ = oracle_penta_sample(args.cpu_budget / 2, 1)
+        vN, used = oracle_penta_sample(args.cpu_budget / 2, cores)
+        va, sa = oracle_adi_sample(args.cpu_budget / 3)
+        cpu = {"value": round(vN / 1e6, 3), "unit": "Munknowns/s", "cores": used, "kind": "oracle",
+               "cpu_model": cpu_model(), "affinity_cores": cores,
+               "sample": f"oracle.penta_batch_solve of 64 of the 8192 systems (N=8192, cyclic, fp64) repeated for "
+                         f"{args.cpu_budget / 2:.0f} s in each of {used} processes (one per host core)",
+               "single_core": {"value": round(v1 / 1e6, 3), "unit": "Munknowns/s", "cores": 1},
+               "ch_adi": {"value": round(va, 3), "unit": "sim-timesteps/s", "sample": sa}}
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(r["value"], 2), "unit": "Munknowns/s", "n_gpus": world,
@@ -441,7 +628,8 @@ def run_ours(args):
                        "layout": "interleaved", "l2": "inputs (512 MiB fp64) larger than the 126 MB L2; no flush",
                        "parallelism": f"independent batches x{world}"},
             "roofline": r["roofline"], "cpu_baseline": cpu, "e2e": r["e2e"], "gpu_launches": r["launches"],
-            "clocks": r["clocks"], "residual": r["residual"], "ch_adi": adi, "dist_adi": dist_adi,
+            "clocks": r["clocks"], "residual": r["residual"], "sweep": sweep, "ch_adi": adi, "cfg3": cfg3,
+            "ch1d": ch1d, "dist_adi": dist_adi,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -451,33 +639,30 @@ def run_ours(args):
 
 def run_reference(args):
     """Reference arm: the CPU oracle as it stands (this tier has no reference
-    implementation), on the same workload/metric, rank 0 only."""
+    implementation), on the same workload/metric, rank 0 only, one process per
+    host core."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import oracle
-    n = PENTA_N
-    m_sample = 64
-    s = synth.SIGMA_STATS
-    diags = synth.const_penta(n, s, -4 * s, 1 + 6 * s, -4 * s, s)
-    f = synth.rhs_uniform(n, m_sample, seed=2)
-    for _ in range(args.warmup):
-        oracle.penta_batch_solve(*diags, f, n=n, m=m_sample, periodic=True)
+    cores = host_cores()
+    per_step = max(0.5, 60.0 / max(args.steps + args.warmup, 1))
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        oracle.penta_batch_solve(*diags, f, n=n, m=m_sample, periodic=True)
+    v, used = oracle_penta_sample(per_step * args.steps, cores)
     el = time.perf_counter() - t0
-    v = n * m_sample * args.steps / el / 1e6
-    sample = f"each step: oracle.penta_batch_solve of {m_sample} of the 8192 systems, N={n} (cyclic, fp64)"
+    sample = (f"oracle.penta_batch_solve of 64 of the 8192 systems (N=8192, cyclic, fp64) repeated in each of {used} "
+              f"processes (one per host core) for {per_step * args.steps:.1f} s")
+    vv = round(v / 1e6, 3)
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "Munknowns/s",
+        "impl": "reference", "metric": METRIC, "value": vv, "unit": "Munknowns/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(PENTA_N * PENTA_N / v * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "configs[1]: batched cyclic penta solve, N=8192, batch=8192 per GPU, "
                                "factor-once/solve-many, interleaved", "N": PENTA_N, "batch_per_gpu": PENTA_N},
-        "cpu_baseline": {"value": round(v, 3), "unit": "Munknowns/s", "cores": 1, "kind": "oracle", "sample": sample},
-        "e2e": {"value": round(v, 3), "unit": "Munknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": vv, "unit": "Munknowns/s", "cores": used, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model()},
+        "e2e": {"value": vv, "unit": "Munknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": round(el, 2),
     }
     print(json.dumps(line), flush=True)
 
@@ -485,18 +670,19 @@ def run_reference(args):
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--adi-steps", type=int, default=None, help="ADI steps timed (default: --steps)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--dtype", choices=["f64", "f32"], default="f64")
     ap.add_argument("--no-adi", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-ch1d", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-dist", action="store_true", help="skip the configs[4] row-partitioned leg (N > 1)")
+    ap.add_argument("--no-dist", action="store_true", help="skip the configs[4] row-partitioned leg")
     ap.add_argument("--dist-n", type=int, default=DIST_N)
-    ap.add_argument("--dist-steps", type=int, default=20)
-    ap.add_argument("--dist-force", action="store_true", help="run the configs[4] leg at N = 1 too (one rank)")
-    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--dist-steps", type=int, default=10)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

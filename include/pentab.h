@@ -114,6 +114,35 @@ PB_API int pent_solve(pb_penta_t h, void *rhs, int layout, void *stream);
 PB_API int pent_solve_many(pb_penta_t h, void *rhs, int layout, int64_t count, int64_t batch_stride,
                     void *stream);
 
+/* pent_solve_strided — the general batched form (systems stored
+ * interleaved, one per thread, or one after another).  System s of batch b
+ * occupies rhs[b*outer_stride + s*inner_stride + i*row_stride], i = 0..n-1,
+ * for s < n_inner and b < n_outer, solved in place.  Examples: interleaved
+ * batch = {M, 1, 1, -, M}; a pitched sub-block of systems [s0, s0+m) of a
+ * wider interleaved array with row pitch P = {m, 1, 1, -, P} at rhs + s0; the
+ * ADI y-sweep of S grids = {n, 1, S, n*n, n}; contiguous rows (the x-sweep) =
+ * {S*n, n, 1, -, 1}.  n_inner must equal the handle's batch for a per-system
+ * LHS (any count for a shared LHS); strides > 0; n_outer <= 65535.
+ * Interleaved (inner_stride 1) or contiguous (row_stride 1) forms with
+ * 16-byte-aligned pitches take the fused streaming solve; other strides are
+ * solved one thread per system.  Errors: PB_EINVAL, PB_ECUDA.             */
+typedef struct {
+    int64_t n_inner;      /* systems per batch                                  */
+    int64_t inner_stride; /* elements between systems s and s+1                 */
+    int64_t n_outer;      /* batches                                            */
+    int64_t outer_stride; /* elements between batches b and b+1                 */
+    int64_t row_stride;   /* elements between unknowns i and i+1 of one system  */
+} pb_layout;
+PB_API int pent_solve_strided(pb_penta_t h, void *rhs, const pb_layout *L, void *stream);
+
+/* pent_solve_info — how the handle's shared-LHS solve resolves the chunk
+ * inflows of the fused streaming solve (diagnostic): *window = L > 0 when the
+ * chunk maps of the factored LHS decay below 1e-18 within L 64-row chunks
+ * (each chunk's inflows then come from its 2L+1 neighbours), 0 when a full
+ * per-group scan is used, -1 when the handle has no fused plan (per-system
+ * LHS or N too large).                                                      */
+PB_API int pent_solve_info(pb_penta_t h, int *window);
+
 PB_API int pent_destroy(pb_penta_t h);
 
 /* ------------------------------------------------------------------------
@@ -127,6 +156,7 @@ PB_API int pent_destroy(pb_penta_t h);
 PB_API int tri_factor(int64_t batch, int64_t n, const double *a, const double *b, const double *c,
                int64_t lhs_count, int periodic, int dtype, void *stream, pb_tri_t *out);
 PB_API int tri_solve(pb_tri_t h, void *rhs, int layout, void *stream);
+PB_API int tri_solve_strided(pb_tri_t h, void *rhs, const pb_layout *L, void *stream);
 PB_API int tri_destroy(pb_tri_t h);
 
 /* ------------------------------------------------------------------------
@@ -166,7 +196,11 @@ PB_API int stencil_apply(const pb_grid *g, const void *in, void *out, const pb_w
  *  s->c_cur, s->c_prev : device pointers to sims*n*n elements ([sim][j][i]);
  *       the caller initialises both to C^0.  On return they point
  *       to the newest / previous level (buffers rotate by pointer swap).
- *  s->work : device scratch of ch_workspace_bytes() bytes, caller-owned.
+ *  s->work : device scratch of ch_workspace_bytes() bytes (fp64 R -> w -> v,
+ *       sims*n*n doubles for either state dtype), caller-owned.
+ *  All three buffers 16-byte aligned.
+ * One step = 4 launches: RHS stencil, x-sweep (fused solve, contiguous rows),
+ * y-sweep (fused solve, interleaved columns, count = sims), combine.
  *  p : D, gamma, L (square periodic domain of side L).
  * L_x = L_y is factored once and cached per (n, dt, D, gamma, L, dtype).
  * Errors: PB_EINVAL (n < 8, bad pointers), PB_ECUDA.                      */
@@ -182,6 +216,32 @@ PB_API int ch_workspace_bytes(int64_t sims, int64_t n, int dtype, size_t *bytes)
 PB_API int ch_adi_step(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nsteps, void *stream);
 
 /* ------------------------------------------------------------------------
+ * ch1d_step — nsteps of the batched 1D Cahn–Hilliard scheme, thesis §6.2
+ * (eq6:1Dnumerical):
+ *   (I + dt gamma d_xxxx) C^{n+1} = C^n + dt d_xx (C^3 - C)^n,  D = 1,
+ * second-order differences on a periodic grid of n points, dx = L/n (r1):
+ * the cyclic pentadiagonal (s, -4s, 1+6s, -4s, s), s = gamma dt/dx^4, and
+ * f_i = C_i + alpha (N_{i-1} - 2 N_i + N_{i+1}), alpha = dt/dx^2,
+ * N = C^3 - C (the +C_i^n term the printed f_i drops, reading r12).
+ *  s->c     device, batch*n elements, interleaved [i*batch + s] (system
+ *           fastest): C^n on entry, C^{n+nsteps} on return.
+ *  s->work  device scratch of the same size; c and work swap each step
+ *           (on return s->c points at the newest level).
+ *  batch must be a multiple of 32; both buffers 16-byte aligned.
+ * The matrix is factored once and cached per (n, dt, gamma, L, dtype).
+ * One kernel launch per step; no host sync.
+ * Errors: PB_EINVAL (sizes, alignment, pointers), PB_ECUDA.               */
+typedef struct {
+    int64_t batch, n;
+    int dtype;
+    void *c, *work;
+} pb_ch1d_state;
+typedef struct {
+    double gamma, L;
+} pb_ch1d_params;
+PB_API int ch1d_step(pb_ch1d_state *s, double dt, const pb_ch1d_params *p, int64_t nsteps, void *stream);
+
+/* ------------------------------------------------------------------------
  * Row-partitioned ADI step (configs[4]: one n x n grid over P ranks,
  * SURVEY §8(e)).  Rank r owns rows [r n/P, (r+1) n/P); one step of Eq 3.1
  * is, per rank (the orchestration and the two all-to-all
@@ -195,24 +255,24 @@ PB_API int ch_adi_step(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t
  * ch_dist_pass_a: cn_ext, cm_ext: device, (rows + 4) x n, rows 2..rows+1 the
  *   rank's rows, rows 0-1 / rows+2..rows+3 the two halo rows of the previous /
  *   next rank (periodic in j across ranks, periodic in i within the row).
- *   w: device rows x n, receives L_x^{-1} R.  dt, p as ch_adi_step.
- * ch_dist_pack: w (rows x n) -> packed [parts][rows][n/parts] (the send layout
- *   of the transpose: column block q contiguous).  n % parts == 0.
- * ch_dist_combine: cm_ext interior rows <- 2 cn_ext - cm_ext + v, with v in
- *   the receive layout [parts][rows][n/parts] (block q = columns of rank q).
+ *   w: device fp64 rows x n (16-byte aligned, n even), receives L_x^{-1} R.
+ *   dt, p as ch_adi_step; dtype = the element type of cn_ext / cm_ext.
+ * ch_dist_pack: fp64 w (rows x n) -> packed [parts][rows][n/parts] (the send
+ *   layout of the transpose: column block q contiguous).  n % parts == 0.
+ * ch_dist_combine: cm_ext interior rows <- 2 cn_ext - cm_ext + v (dtype of
+ *   cn_ext / cm_ext), with fp64 v in the receive layout [parts][rows][n/parts]
+ *   (block q = columns of rank q).
  * All buffers are caller-owned device memory; work is enqueued on stream.
  * Errors: PB_EINVAL (sizes, pointers, dtype), PB_ECUDA.                    */
 PB_API int ch_dist_pass_a(int64_t rows, int64_t n, int dtype, const void *cn_ext, const void *cm_ext, void *w,
                           double dt, const pb_ch_params *p, void *stream);
-PB_API int ch_dist_pack(int64_t rows, int64_t n, int64_t parts, int dtype, const void *w, void *packed,
-                        void *stream);
+PB_API int ch_dist_pack(int64_t rows, int64_t n, int64_t parts, const void *w, void *packed, void *stream);
 /* ch_dist_ysweep: the y-sweep L_y v = w of the rank's column block,
- *   in place: cols is [n][ncols] interleaved (ncols systems of length n, the
- *   receive layout of the first all-to-all), solved with the cyclic L_y of
- *   (n, dt, D, gamma, L) factored once and cached.  ncols * sizeof(T) must be
- *   a multiple of 16 and cols 16-byte aligned (PB_EINVAL otherwise).       */
-PB_API int ch_dist_ysweep(int64_t ncols, int64_t n, int dtype, void *cols, double dt, const pb_ch_params *p,
-                          void *stream);
+ *   in place: cols is fp64 [n][ncols] interleaved (ncols systems of length n,
+ *   the receive layout of the first all-to-all), solved with the cyclic L_y
+ *   of (n, dt, D, gamma, L) factored once and cached.  ncols must be even and
+ *   cols 16-byte aligned (PB_EINVAL otherwise).                           */
+PB_API int ch_dist_ysweep(int64_t ncols, int64_t n, void *cols, double dt, const pb_ch_params *p, void *stream);
 PB_API int ch_dist_combine(int64_t rows, int64_t n, int64_t parts, int dtype, const void *cn_ext, void *cm_ext,
                            const void *v_packed, void *stream);
 

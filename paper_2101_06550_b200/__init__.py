@@ -21,8 +21,8 @@ PB_INTERLEAVED, PB_CONTIGUOUS = 0, 1
 PB_NONPERIODIC, PB_PERIODIC = 0, 1
 
 # every symbol include/pentab.h declares
-EXPORTS = ("pent_factor", "pent_solve", "pent_solve_many", "pent_destroy", "tri_factor", "tri_solve",
-           "tri_destroy", "stencil_apply", "ch_workspace_bytes", "ch_adi_step", "ch_dist_pass_a",
+EXPORTS = ("pent_factor", "pent_solve", "pent_solve_many", "pent_solve_strided", "pent_solve_info", "pent_destroy", "tri_factor",
+           "tri_solve", "tri_solve_strided", "tri_destroy", "stencil_apply", "ch_workspace_bytes", "ch_adi_step", "ch1d_step", "ch_dist_pass_a",
            "ch_dist_pack", "ch_dist_ysweep", "ch_dist_combine", "pb_last_error", "pb_launch_count", "pb_reset_launch_count",
            "pb_device_ok")
 
@@ -31,6 +31,11 @@ class PentabError(RuntimeError):
     def __init__(self, code, msg, sys_idx=-1, row=-1):
         super().__init__(f"pentab error {code}: {msg} (system {sys_idx}, row {row})")
         self.code, self.sys_idx, self.row = code, sys_idx, row
+
+
+class pb_layout(ctypes.Structure):
+    _fields_ = [("n_inner", ctypes.c_int64), ("inner_stride", ctypes.c_int64), ("n_outer", ctypes.c_int64),
+                ("outer_stride", ctypes.c_int64), ("row_stride", ctypes.c_int64)]
 
 
 class pb_grid(ctypes.Structure):
@@ -50,6 +55,15 @@ class pb_ch_params(ctypes.Structure):
     _fields_ = [("D", ctypes.c_double), ("gamma", ctypes.c_double), ("L", ctypes.c_double)]
 
 
+class pb_ch1d_state(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int64), ("n", ctypes.c_int64), ("dtype", ctypes.c_int),
+                ("c", ctypes.c_void_p), ("work", ctypes.c_void_p)]
+
+
+class pb_ch1d_params(ctypes.Structure):
+    _fields_ = [("gamma", ctypes.c_double), ("L", ctypes.c_double)]
+
+
 _lib = None
 
 
@@ -64,6 +78,9 @@ def lib() -> ctypes.CDLL:
         L.pent_factor.argtypes = [I64, I64, P, P, P, P, P, I64, I, I, P, ctypes.POINTER(P)]
         L.pent_solve.argtypes = [P, P, I, P]
         L.pent_solve_many.argtypes = [P, P, I, I64, I64, P]
+        L.pent_solve_strided.argtypes = [P, P, ctypes.POINTER(pb_layout), P]
+        L.tri_solve_strided.argtypes = [P, P, ctypes.POINTER(pb_layout), P]
+        L.pent_solve_info.argtypes = [P, ctypes.POINTER(ctypes.c_int)]
         L.pent_destroy.argtypes = [P]
         L.tri_factor.argtypes = [I64, I64, P, P, P, I64, I, I, P, ctypes.POINTER(P)]
         L.tri_solve.argtypes = [P, P, I, P]
@@ -71,9 +88,10 @@ def lib() -> ctypes.CDLL:
         L.stencil_apply.argtypes = [ctypes.POINTER(pb_grid), P, P, ctypes.POINTER(pb_window), P, I, P]
         L.ch_workspace_bytes.argtypes = [I64, I64, I, ctypes.POINTER(ctypes.c_size_t)]
         L.ch_adi_step.argtypes = [ctypes.POINTER(pb_ch_state), D, ctypes.POINTER(pb_ch_params), I64, P]
+        L.ch1d_step.argtypes = [ctypes.POINTER(pb_ch1d_state), D, ctypes.POINTER(pb_ch1d_params), I64, P]
         L.ch_dist_pass_a.argtypes = [I64, I64, I, P, P, P, D, ctypes.POINTER(pb_ch_params), P]
-        L.ch_dist_pack.argtypes = [I64, I64, I64, I, P, P, P]
-        L.ch_dist_ysweep.argtypes = [I64, I64, I, P, D, ctypes.POINTER(pb_ch_params), P]
+        L.ch_dist_pack.argtypes = [I64, I64, I64, P, P, P]
+        L.ch_dist_ysweep.argtypes = [I64, I64, P, D, ctypes.POINTER(pb_ch_params), P]
         L.ch_dist_combine.argtypes = [I64, I64, I64, I, P, P, P, P]
         L.pb_last_error.argtypes = [ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.c_char_p, ctypes.c_size_t]
         L.pb_launch_count.restype = I64
@@ -128,6 +146,16 @@ def _layout(layout):
 
 class _Banded:
     _destroy = None
+    _strided = None
+
+    def solve_strided(self, rhs, *, n_inner, inner_stride, n_outer=1, outer_stride=0, row_stride, offset=0,
+                      stream=None):
+        """pent_solve_strided / tri_solve_strided (pentab.h): systems at
+        rhs[offset + b*outer_stride + s*inner_stride + i*row_stride], in place."""
+        lay = pb_layout(n_inner, inner_stride, n_outer, outer_stride, row_stride)
+        base = _ptr(rhs).value + offset * (8 if self.dtype == PB_F64 else 4)
+        _check(getattr(lib(), self._strided)(self._h, ctypes.c_void_p(base), ctypes.byref(lay), _stream(rhs, stream)))
+        return rhs
 
     def __init__(self, h, batch, n, dtype):
         self._h, self.batch, self.n, self.dtype = h, batch, n, dtype
@@ -146,11 +174,18 @@ class _Banded:
 
 class PentaHandle(_Banded):
     _destroy = "pent_destroy"
+    _strided = "pent_solve_strided"
 
     def solve(self, rhs, layout="interleaved", stream=None):
         """pent_solve: in place (P:1710-1729)."""
         _check(lib().pent_solve(self._h, _ptr(rhs), _layout(layout), _stream(rhs, stream)))
         return rhs
+
+    def window(self):
+        """pent_solve_info: chunk window of the fused solve (0 = group scan, -1 = none)."""
+        w = ctypes.c_int()
+        _check(lib().pent_solve_info(self._h, ctypes.byref(w)))
+        return w.value
 
     def solve_many(self, rhs, count, batch_stride, layout="interleaved", stream=None):
         _check(lib().pent_solve_many(self._h, _ptr(rhs), _layout(layout), count, batch_stride, _stream(rhs, stream)))
@@ -159,6 +194,7 @@ class PentaHandle(_Banded):
 
 class TriHandle(_Banded):
     _destroy = "tri_destroy"
+    _strided = "tri_solve_strided"
 
     def solve(self, rhs, layout="interleaved", stream=None):
         _check(lib().tri_solve(self._h, _ptr(rhs), _layout(layout), _stream(rhs, stream)))
@@ -241,6 +277,30 @@ def ch_adi_step(state: CHState, dt, *, D=1.0, gamma=0.01, L, nsteps=1, stream=No
     return state
 
 
+class CH1DState:
+    """A batch of 1D CH systems (thesis §6.2): interleaved [n][batch] level +
+    a same-sized work buffer (device tensors); the two swap every step."""
+
+    def __init__(self, c0):
+        import torch
+        assert c0.is_cuda and c0.dim() == 2, "c0: (n, batch) device tensor, system fastest"
+        self.n, self.batch = c0.shape
+        self.dtype = _dtype_code(c0)
+        self.bufs = [c0.clone().contiguous(), torch.empty_like(c0)]
+        self.state = pb_ch1d_state(self.batch, self.n, self.dtype, self.bufs[0].data_ptr(), self.bufs[1].data_ptr())
+
+    @property
+    def c(self):
+        return self.bufs[0] if self.bufs[0].data_ptr() == self.state.c else self.bufs[1]
+
+
+def ch1d_step(state: CH1DState, dt, *, gamma=0.01, L, nsteps=1, stream=None):
+    """nsteps of eq6:1Dnumerical on device; levels swap in `state`."""
+    p = pb_ch1d_params(gamma, L)
+    _check(lib().ch1d_step(ctypes.byref(state.state), dt, ctypes.byref(p), nsteps, _stream(state.bufs[0], stream)))
+    return state
+
+
 def launch_count() -> int:
     return int(lib().pb_launch_count())
 
@@ -257,18 +317,18 @@ def device_ok() -> bool:
 def ch_dist_pass_a(cn_ext, cm_ext, w, *, rows, n, dt, D=1.0, gamma=0.01, L, stream=None):
     """RHS + x-sweep of a row block with 2 halo rows each side (pentab.h)."""
     p = pb_ch_params(D, gamma, L)
-    _check(lib().ch_dist_pass_a(rows, n, _dtype_code(w), _ptr(cn_ext), _ptr(cm_ext), _ptr(w), dt, ctypes.byref(p),
+    _check(lib().ch_dist_pass_a(rows, n, _dtype_code(cn_ext), _ptr(cn_ext), _ptr(cm_ext), _ptr(w), dt, ctypes.byref(p),
                                 _stream(w, stream)))
 
 
 def ch_dist_pack(w, packed, *, rows, n, parts, stream=None):
-    _check(lib().ch_dist_pack(rows, n, parts, _dtype_code(w), _ptr(w), _ptr(packed), _stream(w, stream)))
+    _check(lib().ch_dist_pack(rows, n, parts, _ptr(w), _ptr(packed), _stream(w, stream)))
 
 
 def ch_dist_ysweep(cols, *, ncols, n, dt, D=1.0, gamma=0.01, L, stream=None):
     """y-sweep of the rank's [n][ncols] column block, in place (pentab.h)."""
     p = pb_ch_params(D, gamma, L)
-    _check(lib().ch_dist_ysweep(ncols, n, _dtype_code(cols), _ptr(cols), dt, ctypes.byref(p), _stream(cols, stream)))
+    _check(lib().ch_dist_ysweep(ncols, n, _ptr(cols), dt, ctypes.byref(p), _stream(cols, stream)))
 
 
 def ch_dist_combine(cn_ext, cm_ext, v_packed, *, rows, n, parts, stream=None):

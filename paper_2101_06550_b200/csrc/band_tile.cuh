@@ -24,14 +24,15 @@ struct Plan {
 struct FusedScratch {
     void *buf = nullptr;
     size_t bytes = 0;
-    unsigned epoch = 0;
     int64_t nq = 0, nsys = 0;
-    // the last tensor map encoded for this stream (rhs pointer + shape key)
-    uint64_t key[6] = {0, 0, 0, 0, 0, 0};
-    alignas(64) unsigned char tmap[128];
+    // the last tensor map encoded for this stream, per layout (rhs pointer + shape key)
+    uint64_t key[2][6] = {{0, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0}};
+    alignas(64) unsigned char tmap[2][128];
 };
 struct FusedPlan {
     int ok = 0, nq = 0;
+    int win = 0;                        // windowed inflows over 2*win+1 chunks (0: group scan)
+    unsigned char *needxl = nullptr;    // [nq] chunk carries a cyclic correction (device)
     void *rec = nullptr, *ct = nullptr, *rsp = nullptr;
     mutable std::mutex mu;
     mutable std::map<cudaStream_t, FusedScratch> scratch;
@@ -66,6 +67,7 @@ struct Band {
         cudaFree(fplan.rec);
         cudaFree(fplan.ct);
         cudaFree(fplan.rsp);
+        cudaFree(fplan.needxl);
         for (auto &kv : fplan.scratch) {
             cudaStreamSynchronize(kv.first);
             cudaFree(kv.second.buf);
@@ -223,9 +225,21 @@ static int launch_tile_l(const Band *h, T *x, int layout, int64_t count, int64_t
 int const_penta_band(int64_t n, double sigma, int dtype, int cfg, int C, cudaStream_t st, Band **out);
 
 int fused_build_tables(Band *h, cudaStream_t st);
-// shared-LHS interleaved solve of `count` batches (batch k at x + k * bstride
-// elements); M = systems per batch (0: the handle's batch)
-int launch_fused(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st, int64_t M = 0);
+// after the factor's sync: choose windowed or group-scan inflows from the decay
+// of the chunk maps, and mark the chunks that carry a cyclic correction
+int fused_window_plan(Band *h);
+// the dispatching solves behind pent_solve / pent_solve_many / pent_solve_strided / tri_*
+int band_solve(const Band *h, void *rhs, int layout, int64_t count, int64_t bstride, cudaStream_t st);
+int band_solve_layout(const Band *h, void *rhs, const pb_layout &L, cudaStream_t st);
+// shared-LHS solve of `count` batches (batch k at x + k * bstride elements) in
+// `layout` (PB_INTERLEAVED / PB_CONTIGUOUS); M = systems per batch (0: the
+// handle's); pitch = elements between rows (interleaved) / systems (contiguous),
+// 0 = packed
+int launch_fused(const Band *h, void *x, int layout, int64_t count, int64_t bstride, cudaStream_t st, int64_t M = 0,
+                 int64_t pitch = 0);
+// one step of the batched 1D Cahn–Hilliard scheme (fused_solve.cuh MODE_CH1D):
+// c -> cnew, M interleaved systems, alpha = dt/dx^2, h = the cyclic (s,-4s,1+6s,-4s,s)
+int launch_fused_ch1d(const Band *h, const void *c, void *cnew, double alpha, int64_t M, cudaStream_t st);
 
 // per-(dtype, K) entry points, defined in banded_inst_*.cu
 int launch_tile_f64_k2(const Band *h, void *x, int layout, int64_t count, int64_t bstride, cudaStream_t st);

@@ -7,6 +7,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include <cudaTypedefs.h>
@@ -337,15 +338,16 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
 
 // ---------------------------------------------------------------- one thread per system
 // The thesis's cuPentBatch kernel shape: g stored in place.
-// Used for per-system LHS and for shared LHS beyond the cluster capacity.
+// Used for per-system LHS and for any strides the fused solve cannot take:
+// element i of system s of batch b at x[b*bstride + s*xs + i*xr].
 template <typename T, int K, bool PER>
 __global__ void band_persys_kernel(T *x, const T *coef, int64_t cstr, const double *scal, int64_t sstr,
-                                   int64_t N, int64_t M, int layout, int64_t bstride)
+                                   int64_t N, int64_t M, int64_t xs, int64_t xr, int64_t bstride)
 {
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s >= M) return;
     T *X = x + (int64_t)blockIdx.y * bstride;
-    auto IX = [&](int64_t i) -> int64_t { return layout == PB_INTERLEAVED ? i * M + s : s * N + i; };
+    auto IX = [&](int64_t i) -> int64_t { return s * xs + i * xr; };
     const int64_t cmul = cstr ? cstr : 1;
     auto CG = [&](int64_t i, int j) -> T { return coef[(i * COEF_STRIDE + j) * cmul + (cstr ? s : 0)]; };
     T y0 = 0, y1 = 0, sp[4] = {0, 0, 0, 0};
@@ -439,7 +441,7 @@ static int choose_cfg(int64_t n, int64_t batch, int dtype, int *C_out)
 }
 
 template <typename T, int K>
-static int launch_persys_t(const Band *h, T *x, int layout, int64_t count, int64_t bstride, cudaStream_t st)
+static int launch_persys_t(const Band *h, T *x, const pb_layout &L, cudaStream_t st)
 {
     const bool shared = h->shared();
     const T *coef = (const T *)(shared ? h->coef : h->pcoef);
@@ -447,11 +449,13 @@ static int launch_persys_t(const Band *h, T *x, int layout, int64_t count, int64
     const double *scal = shared ? h->scal : h->pscal;
     const int64_t sstr = shared ? 0 : h->batch;
     const int nt = 128;
-    dim3 grid((unsigned)((h->batch + nt - 1) / nt), (unsigned)count);
+    dim3 grid((unsigned)((L.n_inner + nt - 1) / nt), (unsigned)L.n_outer);
     if (h->periodic)
-        band_persys_kernel<T, K, true><<<grid, nt, 0, st>>>(x, coef, cstr, scal, sstr, h->n, h->batch, layout, bstride);
+        band_persys_kernel<T, K, true><<<grid, nt, 0, st>>>(x, coef, cstr, scal, sstr, h->n, L.n_inner, L.inner_stride,
+                                                            L.row_stride, L.outer_stride);
     else
-        band_persys_kernel<T, K, false><<<grid, nt, 0, st>>>(x, coef, cstr, scal, sstr, h->n, h->batch, layout, bstride);
+        band_persys_kernel<T, K, false><<<grid, nt, 0, st>>>(x, coef, cstr, scal, sstr, h->n, L.n_inner, L.inner_stride,
+                                                             L.row_stride, L.outer_stride);
     PB_LAUNCH_CHECK();
     return PB_OK;
 }
@@ -582,44 +586,130 @@ static int factor_impl(Band *h, const double *a, const double *b, const double *
         set_pivot(sys, -1);
         return code;
     }
+    if (h->shared()) return fused_window_plan(h);
     return PB_OK;
 }
 
-static int solve_impl(const Band *h, void *rhs, int layout, int64_t count, int64_t bstride, cudaStream_t st)
+// Host right-hand sides (interleaved, one batch, shared LHS): the systems are
+// cut into NCHUNK column blocks and pipelined over two internal streams --
+// pitched H2D copy of block c+1 | fused solve of block c | pitched D2H of
+// block c-1 -- so both PCIe directions and the solve overlap.  The caller's
+// stream is joined at the start and the end; the call returns with the host
+// buffer updated (the host-buffer contract of pentab.h).
+static int pipelined_host_solve(const Band *h, void *host, const pb_layout &L, cudaStream_t st)
+{
+    constexpr int NCHUNK = 8;
+    const size_t es = dtype_size(h->dtype);
+    const int64_t n = h->n, M = L.n_inner, P = L.row_stride;
+    int64_t mc = (M + NCHUNK - 1) / NCHUNK;
+    mc = (mc + 31) / 32 * 32;   // whole 32-system tiles, 16-byte pitch
+    const int nch = (int)((M + mc - 1) / mc);
+    struct Res {
+        cudaStream_t s[2] = {nullptr, nullptr};
+        cudaEvent_t e[3] = {nullptr, nullptr, nullptr};
+        void *buf[2] = {nullptr, nullptr};
+        cudaStream_t owner = nullptr;
+        ~Res()
+        {
+            for (int k = 0; k < 2; ++k)
+                if (buf[k]) cudaFreeAsync(buf[k], owner);
+            for (auto ev : e)
+                if (ev) cudaEventDestroy(ev);
+            for (auto x : s)
+                if (x) cudaStreamDestroy(x);
+        }
+    } R;
+    R.owner = st;
+    for (int k = 0; k < 2; ++k) PB_CUDA_TRY(cudaStreamCreateWithFlags(&R.s[k], cudaStreamNonBlocking));
+    for (int k = 0; k < 3; ++k) PB_CUDA_TRY(cudaEventCreateWithFlags(&R.e[k], cudaEventDisableTiming));
+    const size_t cbytes = es * (size_t)mc * (size_t)n;
+    for (int k = 0; k < 2; ++k) PB_CUDA_TRY(cudaMallocAsync(&R.buf[k], cbytes, st));
+    PB_CUDA_TRY(cudaEventRecord(R.e[2], st));   // the caller's prior work (and the allocations)
+    for (int k = 0; k < 2; ++k) PB_CUDA_TRY(cudaStreamWaitEvent(R.s[k], R.e[2], 0));
+    char *hb = (char *)host;
+    for (int c = 0; c < nch; ++c) {
+        const int k = c & 1;
+        const int64_t s0 = (int64_t)c * mc, m = std::min<int64_t>(mc, M - s0);
+        // block c reuses buffer k after block c-2's D2H (same stream: ordered)
+        PB_CUDA_TRY(cudaMemcpy2DAsync(R.buf[k], es * m, hb + es * s0, es * P, es * m, n, cudaMemcpyHostToDevice, R.s[k]));
+        int rc = launch_fused(h, R.buf[k], PB_INTERLEAVED, 1, 0, R.s[k], m, m);
+        if (rc) return rc;
+        PB_CUDA_TRY(cudaMemcpy2DAsync(hb + es * s0, es * P, R.buf[k], es * m, es * m, n, cudaMemcpyDeviceToHost, R.s[k]));
+    }
+    for (int k = 0; k < 2; ++k) {
+        PB_CUDA_TRY(cudaEventRecord(R.e[k], R.s[k]));
+        PB_CUDA_TRY(cudaStreamWaitEvent(st, R.e[k], 0));
+    }
+    PB_CUDA_TRY(cudaStreamSynchronize(st));
+    return PB_OK;
+}
+
+// The general solve: systems (s, b) at rhs + b*outer_stride + s*inner_stride,
+// unknown i at + i*row_stride.  Shared LHS with either packed or
+// pitched interleaved (inner_stride 1) or contiguous (row_stride 1) systems ->
+// the fused streaming solve; packed layouts with unaligned buffers -> the
+// register-tile kernel; anything else (and per-system LHS) -> one thread per
+// system.  Host buffers are staged through device scratch (Staged).
+int band_solve_layout(const Band *h, void *rhs, const pb_layout &L, cudaStream_t st)
+{
+    if (!h) return set_error(PB_EINVAL, "null handle");
+    if (L.n_inner < 0 || L.n_outer < 0 || L.n_outer > 65535) return set_error(PB_EINVAL, "bad system / batch count");
+    if (L.n_inner == 0 || L.n_outer == 0 || h->batch == 0) return PB_OK;
+    if (!h->shared() && L.n_inner != h->batch) return set_error(PB_EINVAL, "per-system LHS: n_inner must equal batch");
+    if (L.inner_stride < 1 || L.row_stride < 1 || (L.n_outer > 1 && L.outer_stride < 1))
+        return set_error(PB_EINVAL, "strides must be positive");
+    const int64_t n = h->n;
+    const bool inter = L.inner_stride == 1 && L.row_stride >= L.n_inner;
+    const bool contig = L.row_stride == 1 && L.inner_stride >= n;
+    const size_t es = dtype_size(h->dtype);
+    if (inter && L.n_outer == 1 && h->shared() && h->fplan.ok && L.n_inner >= 4096 && !is_device_ptr(rhs))
+        return pipelined_host_solve(h, rhs, L, st);
+    const int64_t span = (L.n_outer - 1) * L.outer_stride + (L.n_inner - 1) * L.inner_stride + (n - 1) * L.row_stride + 1;
+    Staged sx;
+    int rc = sx.in(rhs, es * (size_t)span, st, true);
+    if (rc) return rc;
+    sx.out_to(rhs);
+    const bool a16 = (uintptr_t)sx.dev % 16 == 0 && (L.n_outer == 1 || (L.outer_stride * es) % 16 == 0);
+    const bool fused = h->shared() && h->fplan.ok && a16 &&
+                       ((inter && (L.row_stride * es) % 16 == 0) || (contig && (L.inner_stride * es) % 16 == 0));
+    const bool packed = L.n_inner == h->batch && ((inter && L.row_stride == L.n_inner) || (contig && L.inner_stride == n)) &&
+                        (L.n_outer == 1 || L.outer_stride >= L.n_inner * n);
+    if (fused) {
+        rc = launch_fused(h, sx.dev, inter ? PB_INTERLEAVED : PB_CONTIGUOUS, L.n_outer, L.outer_stride, st, L.n_inner,
+                          inter ? L.row_stride : L.inner_stride);
+    } else if (h->shared() && h->plan.C > 0 && packed) {
+        const int layout = inter ? PB_INTERLEAVED : PB_CONTIGUOUS;
+        rc = h->dtype == PB_F64
+                 ? (h->K == 2 ? launch_tile_f64_k2(h, sx.dev, layout, L.n_outer, L.outer_stride, st)
+                              : launch_tile_f64_k1(h, sx.dev, layout, L.n_outer, L.outer_stride, st))
+                 : (h->K == 2 ? launch_tile_f32_k2(h, sx.dev, layout, L.n_outer, L.outer_stride, st)
+                              : launch_tile_f32_k1(h, sx.dev, layout, L.n_outer, L.outer_stride, st));
+    } else if (h->dtype == PB_F64) {
+        rc = h->K == 2 ? launch_persys_t<double, 2>(h, (double *)sx.dev, L, st)
+                       : launch_persys_t<double, 1>(h, (double *)sx.dev, L, st);
+    } else {
+        rc = h->K == 2 ? launch_persys_t<float, 2>(h, (float *)sx.dev, L, st)
+                       : launch_persys_t<float, 1>(h, (float *)sx.dev, L, st);
+    }
+    if (rc) return rc;
+    return sx.finish();
+}
+
+// the packed layouts of pent_solve / pent_solve_many / tri_solve
+int band_solve(const Band *h, void *rhs, int layout, int64_t count, int64_t bstride, cudaStream_t st)
 {
     if (!h) return set_error(PB_EINVAL, "null handle");
     if (layout != PB_INTERLEAVED && layout != PB_CONTIGUOUS) return set_error(PB_EINVAL, "bad layout");
     if (count < 0 || count > 65535) return set_error(PB_EINVAL, "bad count");
-    if (h->batch == 0 || count == 0) return PB_OK;
-    const size_t es = dtype_size(h->dtype);
     const int64_t per = h->batch * h->n;
     if (count > 1 && bstride < per) return set_error(PB_EINVAL, "batch_stride < batch*n");
-    const size_t bytes = es * (size_t)((count - 1) * bstride + per);
-    Staged sx;
-    int rc = sx.in(rhs, bytes, st, true);
-    if (rc) return rc;
-    sx.out_to(rhs);
-    const bool al = (uintptr_t)sx.dev % 16 == 0 && (h->batch * es) % 16 == 0 && (count == 1 || (bstride * es) % 16 == 0);
-    // interleaved shared-LHS solve: the fused streaming solve (fused_solve.cuh);
-    // the register-tile kernel serves the contiguous layout and unaligned buffers,
-    // one thread per system serves per-system LHS
-    const bool inter = h->shared() && layout == PB_INTERLEAVED && al;
-    if (inter && h->fplan.ok)
-        rc = launch_fused(h, sx.dev, count, bstride, st);
-    else if (h->shared() && h->plan.C > 0)
-        rc = h->dtype == PB_F64
-                 ? (h->K == 2 ? launch_tile_f64_k2(h, sx.dev, layout, count, bstride, st)
-                              : launch_tile_f64_k1(h, sx.dev, layout, count, bstride, st))
-                 : (h->K == 2 ? launch_tile_f32_k2(h, sx.dev, layout, count, bstride, st)
-                              : launch_tile_f32_k1(h, sx.dev, layout, count, bstride, st));
-    else if (h->dtype == PB_F64)
-        rc = h->K == 2 ? launch_persys_t<double, 2>(h, (double *)sx.dev, layout, count, bstride, st)
-                       : launch_persys_t<double, 1>(h, (double *)sx.dev, layout, count, bstride, st);
-    else
-        rc = h->K == 2 ? launch_persys_t<float, 2>(h, (float *)sx.dev, layout, count, bstride, st)
-                       : launch_persys_t<float, 1>(h, (float *)sx.dev, layout, count, bstride, st);
-    if (rc) return rc;
-    return sx.finish();
+    pb_layout L;
+    L.n_inner = h->batch;
+    L.n_outer = count;
+    L.outer_stride = count > 1 ? bstride : per;
+    L.inner_stride = layout == PB_INTERLEAVED ? 1 : h->n;
+    L.row_stride = layout == PB_INTERLEAVED ? h->batch : 1;
+    return band_solve_layout(h, rhs, L, st);
 }
 
 template <typename H>
@@ -700,12 +790,25 @@ int pent_factor(int64_t batch, int64_t n, const double *a, const double *b, cons
 
 int pent_solve(pb_penta_t h, void *rhs, int layout, void *stream)
 {
-    return pb::solve_impl(h, rhs, layout, 1, 0, (cudaStream_t)stream);
+    return pb::band_solve(h, rhs, layout, 1, 0, (cudaStream_t)stream);
 }
 
 int pent_solve_many(pb_penta_t h, void *rhs, int layout, int64_t count, int64_t batch_stride, void *stream)
 {
-    return pb::solve_impl(h, rhs, layout, count, batch_stride, (cudaStream_t)stream);
+    return pb::band_solve(h, rhs, layout, count, batch_stride, (cudaStream_t)stream);
+}
+
+int pent_solve_strided(pb_penta_t h, void *rhs, const pb_layout *L, void *stream)
+{
+    if (!L) return pb::set_error(PB_EINVAL, "null layout");
+    return pb::band_solve_layout(h, rhs, *L, (cudaStream_t)stream);
+}
+
+int pent_solve_info(pb_penta_t h, int *window)
+{
+    if (!h || !window) return pb::set_error(PB_EINVAL, "null argument");
+    *window = (h->shared() && h->fplan.ok) ? h->fplan.win : -1;
+    return PB_OK;
 }
 
 int pent_destroy(pb_penta_t h)
@@ -722,7 +825,13 @@ int tri_factor(int64_t batch, int64_t n, const double *a, const double *b, const
 
 int tri_solve(pb_tri_t h, void *rhs, int layout, void *stream)
 {
-    return pb::solve_impl(h, rhs, layout, 1, 0, (cudaStream_t)stream);
+    return pb::band_solve(h, rhs, layout, 1, 0, (cudaStream_t)stream);
+}
+
+int tri_solve_strided(pb_tri_t h, void *rhs, const pb_layout *L, void *stream)
+{
+    if (!L) return pb::set_error(PB_EINVAL, "null layout");
+    return pb::band_solve_layout(h, rhs, *L, (cudaStream_t)stream);
 }
 
 int tri_destroy(pb_tri_t h)

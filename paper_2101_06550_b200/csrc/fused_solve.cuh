@@ -26,12 +26,16 @@
 //             window of f fits in L2 -> HBM traffic = read f once + write x once.
 //
 // Work order.  Items are numbered in one global order: for s = 0, 1, ...:
-// the nq P1 tiles of group s, then the nq P2 tiles of group s - D.  CTAs CLAIM
-// items NC at a time from a global ticket (one per consumer warp), so every
-// claimed item precedes every unclaimed one: the earliest incomplete item
-// never waits on anything later (P1 waits on nothing; P2(g) waits only on the
-// scan of g, whose P1 tiles all precede it and whose scan team, claimed in
-// group order, waits only on those) -> no deadlock, whatever the residency.
+// the nq P1 tiles of group s, then the nq P2 tiles of group s - D.  Claims of
+// NC consecutive items (one per consumer warp) are dealt round-robin to the
+// CTAs (claim c -> CTA c mod grid), and every CTA, warp and scan team works
+// through its share in that order.  The launch is cooperative, so all CTAs are
+// co-resident, and the earliest incomplete item never waits on anything later
+// (P1 waits on nothing; P2(g) waits only on the scan of g, whose P1 tiles all
+// precede it and whose scan team -- groups dealt round-robin, in order --
+// waits only on earlier groups' P1 tiles) -> no deadlock.  (A dynamic ticket
+// gives the same guarantee without co-residency, but 16 K same-address
+// atomics per solve serialise at ~45 ns each on B200: measured 759 us.)
 //
 // Per CTA: 1 producer warp (claims, flags, TMA), NC consumer warps, NSW scan
 // warps.  Ring of NS slots (NS a multiple of NC): local item j goes to warp
@@ -61,6 +65,15 @@ constexpr int REC = 6;   // P1 row record length
 constexpr int NC = 4;    // consumer warps (= items per claim)
 constexpr int NSW = 3;   // scan warps (1 + NC + NSW = 8 warps: the full 255-register budget)
 constexpr int NTHREADS = 32 * (NC + 1 + NSW);
+constexpr int LMAX = 3;  // windowed mode: the chunk maps of the LHS decay below 1e-18 within LMAX chunks
+
+// what the tile holds on arrival:
+//   MODE_SOLVE  the right-hand side f (pent_solve / tri_solve / the ADI y-sweep)
+//   MODE_CH1D   the 1D Cahn–Hilliard level C^n; f is formed on chip from the
+//               tile and its two halo rows (eq6:1Dnumerical):
+//               f_i = C_i + alpha (N_{i-1} - 2 N_i + N_{i+1}), N = C^3 - C
+//               (the +C_i^n term of reading r12), and x = C^{n+1} goes to xout
+constexpr int MODE_SOLVE = 0, MODE_CH1D = 1;
 template <typename T>
 constexpr int sbatch() { return 8; }   // scan records per register batch
 
@@ -68,9 +81,12 @@ template <typename T>
 struct Cfg {
     static constexpr int TILE = Q * TW;             // elements
     static constexpr int COEF = Q * COEF_STRIDE;    // >= Q * REC
-    static constexpr int INF = TW * 4;              // (yin0, yin1, zin0, zin1) per lane
+    // inflow area: group-scan mode (yin, zin) blocks of 32 systems x 2, or
+    // windowed mode 2*LMAX yF blocks + LMAX zB blocks (chunk records, pairs)
+    static constexpr int INF = 3 * LMAX * TW * 2;
     static constexpr int XL = TW * 2;
-    static constexpr int SLOT = TILE + COEF + INF + XL;
+    static constexpr int HALO = TW * 2;             // MODE_CH1D: rows r0 - 1 and r0 + kmax (periodic)
+    static constexpr int SLOT = TILE + COEF + INF + XL + HALO;
     static constexpr int NS = sizeof(T) == 8 ? 8 : 16;
     static_assert(NS % NC == 0, "ring slots must be a multiple of the consumer warps");
 };
@@ -79,21 +95,28 @@ template <typename T>
 struct Args {
     const T *rec, *coef, *ct, *rsp;
     const double *scal;
-    T *car;             // [q][sys][4]: P1 (yF, zB) -> scan (yin, zin)
+    T *car;             // chunk records [q][half][sys][2]: half 0 = yF (-> yin), half 1 = zB (-> zin)
     T *spec;            // [sys][4] zero-inflow g on the cyclic rows
     T *xl;              // [sys][2]
-    T *x;               // the right-hand sides, solved in place
+    T *x;               // the right-hand sides (MODE_SOLVE: solved in place; MODE_CH1D: C^n)
+    T *xout;            // where P2 writes x (== x for MODE_SOLVE; C^{n+1} for MODE_CH1D)
+    T alpha;            // MODE_CH1D: dt / dx^2
     int64_t bstride;    // elements between batches
-    unsigned *cnt;      // [G] P1 tiles done (reset by the scan team)
-    unsigned *flag;     // [G] == epoch once the group is scanned
-    unsigned *tick;     // [0] item claims, [1] scan claims, [2] CTAs done (reset by the last CTA)
-    unsigned epoch;
+    int64_t pitch;      // interleaved: elements between rows (>= M); contiguous: between systems (>= n)
+    unsigned *cnt;      // [G] P1 tiles done, cumulative over launches (== epoch * nq when complete)
+    unsigned *flag;     // [G] == this launch's epoch once the group is scanned
+    unsigned *tick;     // [2] CTAs done (reset by the last CTA), [3] launches completed: this
+                        // launch's epoch is tick[3] + 1 (kept on the device, so a solve captured
+                        // in a CUDA graph is correct on every replay)
     int64_t n, M, nsys; // rows, systems per batch, padded systems over all batches (= 32 G)
     int64_t items, nclaims;
     int64_t srow[4];
     int nq, count, Gb, G, D;
     int qspec;          // first chunk holding a cyclic row (cyclic only)
-    int flat;           // batches contiguous and n % Q == 0: 2-D maps, row = b * n + r
+    int win;            // windowed mode: inflows from the 2*win+1 neighbouring chunks (0: group scan)
+    const unsigned char *needxl;   // windowed + cyclic: chunk q's rows carry a cyclic correction
+    int flat;           // one 2-D map over all batches: interleaved (M, n*count), row b*n + r (n % Q == 0);
+                        // contiguous (n, M*count), system b*M + s (M % 32 == 0)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -157,6 +180,18 @@ __device__ __forceinline__ void tma_load2(void *dst, const CUtensorMap *m, int c
         "l"(m), "r"(c0), "r"(c1), "r"(su32(bar)), "l"(pol)
         : "memory");
 }
+__device__ __forceinline__ void tma_store2(const CUtensorMap *m, int c0, int c1, const void *src)
+{
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(m), "r"(c0), "r"(c1),
+                 "r"(su32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store3(const CUtensorMap *m, int c0, int c1, int c2, const void *src)
+{
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(m), "r"(c0),
+                 "r"(c1), "r"(c2), "r"(su32(src))
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
 {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -213,11 +248,54 @@ __device__ __forceinline__ Item decode(int64_t i, int nq, int G, int D)
     return it;
 }
 
+// chunk record (q, sys): half 0 = (yF0, yF1) / (yin0, yin1), half 1 = (zB0, zB1)
+// / (zin0, zin1); the 32 systems of a group are contiguous per (q, half)
+__device__ __forceinline__ int64_t rec_off(int64_t q, int half, int64_t sys, int64_t nsys)
+{
+    return ((2 * q + half) * nsys + sys) * 2;
+}
+
+// ---------------------------------------------------------------- tile layouts in the slot
+// LAY_INTER  (interleaved rhs, x[i*M + s]): the TMA box (32 systems, 64 rows)
+//            lands as [row][lane] -> element (k, lane) at k*TW + lane.
+// LAY_CONTIG (contiguous rhs, x[s*n + i]; the ADI x-sweep): the tile is EB =
+//            128/sizeof(T) rows x 32 systems per TMA box (Q/EB boxes), box
+//            rows = systems, 128B-swizzled: the 16-byte unit u of system s is
+//            stored at unit u ^ (s & 7), so the 32 lanes reading the same row k
+//            of their own system hit 8 distinct unit groups per 8 lanes
+//            (conflict-free 16-byte reads, 4 wavefronts per warp).
+constexpr int LAY_INTER = 0, LAY_CONTIG = 1;
+
+template <typename T>
+struct Sw {
+    static constexpr int EB = 128 / (int)sizeof(T);   // rows per box (one 128-byte box row per system)
+    static constexpr int EU = 16 / (int)sizeof(T);    // elements per 16-byte unit
+};
+// element offset of (row k, system lane) in a LAY_CONTIG tile
+template <typename T>
+__device__ __forceinline__ int csw(int k, int lane)
+{
+    constexpr int EB = Sw<T>::EB, EU = Sw<T>::EU;
+    const int b = k / EB, kk = k % EB;
+    return b * (TW * EB) + lane * EB + (((kk / EU) ^ (lane & 7)) * EU) + kk % EU;
+}
+template <typename T, int LAY>
+__device__ __forceinline__ T tld(const T *d, int k, int lane)
+{
+    return LAY == LAY_INTER ? d[k * TW + lane] : d[csw<T>(k, lane)];
+}
+template <typename T, int LAY>
+__device__ __forceinline__ void tst(T *d, int k, int lane, T v)
+{
+    if (LAY == LAY_INTER) d[k * TW + lane] = v;
+    else d[csw<T>(k, lane)] = v;
+}
+
 // ---------------------------------------------------------------- tile kernels (one warp)
 // P1: zero-inflow forward sweep, carry and back-substitution functional.
 // FULL: kmax == Q (no row guards); SPEC: the tile holds cyclic rows (ks[j] =
 // row srow[j] - r0 inside the tile, else -1)
-template <typename T, int K, bool SPEC, bool FULL>
+template <typename T, int K, bool SPEC, bool FULL, int LAY>
 __device__ __forceinline__ void tile_carry(const T *d, const T *c, int kmax, int lane, const int (&ks)[4],
                                            const Args<T> &A, int64_t sys, bool ok, int q)
 {
@@ -228,7 +306,7 @@ __device__ __forceinline__ void tile_carry(const T *d, const T *c, int kmax, int
         lds2(c + k * REC, f0, f1);
         lds2(c + k * REC + 2, f2, wa);
         const T wb = c[k * REC + 4];
-        T g = f0 * d[k * TW + lane] - f1 * y1;
+        T g = f0 * tld<T, LAY>(d, k, lane) - f1 * y1;
         if (K == 2) g -= f2 * y0;
         y0 = y1;
         y1 = g;
@@ -241,11 +319,12 @@ __device__ __forceinline__ void tile_carry(const T *d, const T *c, int kmax, int
         }
     }
     if (ok) {
-        T *o = A.car + ((int64_t)q * A.nsys + sys) * 4;
+        T *o = A.car + rec_off(q, 0, sys, A.nsys);
+        T *o2 = A.car + rec_off(q, 1, sys, A.nsys);
         o[0] = y0;
         o[1] = y1;
-        o[2] = a0;
-        o[3] = a1;
+        o2[0] = a0;
+        o2[1] = a1;
     }
 }
 
@@ -311,25 +390,34 @@ __device__ __forceinline__ void ldm4(const T *p, T *m)
     m[0] = __ldg(p), m[1] = __ldg(p + 1), m[2] = __ldg(p + 2), m[3] = __ldg(p + 3);
 }
 template <typename T>
-__device__ __forceinline__ void ld_rec(const T *p, T *r)
+__device__ __forceinline__ void ld_pair(const T *p, T &a, T &b)
 {
     if (sizeof(T) == 8) {
-        const double2 u = __ldcg(reinterpret_cast<const double2 *>(p)), w = __ldcg(reinterpret_cast<const double2 *>(p + 2));
-        r[0] = (T)u.x, r[1] = (T)u.y, r[2] = (T)w.x, r[3] = (T)w.y;
+        const double2 u = __ldcg(reinterpret_cast<const double2 *>(p));
+        a = (T)u.x, b = (T)u.y;
     } else {
-        const float4 u = __ldcg(reinterpret_cast<const float4 *>(p));
-        r[0] = (T)u.x, r[1] = (T)u.y, r[2] = (T)u.z, r[3] = (T)u.w;
+        const float2 u = __ldcg(reinterpret_cast<const float2 *>(p));
+        a = (T)u.x, b = (T)u.y;
     }
 }
 template <typename T>
-__device__ __forceinline__ void st_rec(T *p, const T *r)
+__device__ __forceinline__ void st_pair(T *p, T a, T b)
 {
-    if (sizeof(T) == 8) {
-        __stcg(reinterpret_cast<double2 *>(p), make_double2((double)r[0], (double)r[1]));
-        __stcg(reinterpret_cast<double2 *>(p + 2), make_double2((double)r[2], (double)r[3]));
-    } else {
-        __stcg(reinterpret_cast<float4 *>(p), make_float4((float)r[0], (float)r[1], (float)r[2], (float)r[3]));
-    }
+    if (sizeof(T) == 8) __stcg(reinterpret_cast<double2 *>(p), make_double2((double)a, (double)b));
+    else __stcg(reinterpret_cast<float2 *>(p), make_float2((float)a, (float)b));
+}
+// record (q, sys) -> r[0..3] = (half 0, half 1)
+template <typename T>
+__device__ __forceinline__ void ld_rec(const Args<T> &A, int64_t q, int64_t sys, T *r)
+{
+    ld_pair(A.car + rec_off(q, 0, sys, A.nsys), r[0], r[1]);
+    ld_pair(A.car + rec_off(q, 1, sys, A.nsys), r[2], r[3]);
+}
+template <typename T>
+__device__ __forceinline__ void st_rec(const Args<T> &A, int64_t q, int64_t sys, const T *r)
+{
+    st_pair(A.car + rec_off(q, 0, sys, A.nsys), r[0], r[1]);
+    st_pair(A.car + rec_off(q, 1, sys, A.nsys), r[2], r[3]);
 }
 
 template <typename T>
@@ -351,8 +439,6 @@ __device__ void scan_group(const Args<T> &A, ScanSmem<T> &S, int g, int sw, int 
     const int64_t sys = (int64_t)g * TW + lane;
     const int nq = A.nq, cps = (nq + NSW - 1) / NSW;
     const int qa = min(nq, sw * cps), qe = min(nq, qa + cps);
-    T *car = A.car + sys * 4;
-    const int64_t qstride = A.nsys * 4;
     constexpr int SB = sbatch<T>();
 
     // ---- forward fold of my segment: a = (Mf a + yF) over q, P = prod Mf
@@ -361,7 +447,7 @@ __device__ void scan_group(const Args<T> &A, ScanSmem<T> &S, int g, int sw, int 
         T R[SB][4];
 #pragma unroll
         for (int i = 0; i < SB; ++i)
-            if (q0 + i < qe) ld_rec(car + (q0 + i) * qstride, R[i]);
+            if (q0 + i < qe) ld_rec(A, q0 + i, sys, R[i]);
 #pragma unroll
         for (int i = 0; i < SB; ++i)
             if (q0 + i < qe) {
@@ -390,7 +476,7 @@ __device__ void scan_group(const Args<T> &A, ScanSmem<T> &S, int g, int sw, int 
         T R[SB][4];
 #pragma unroll
         for (int i = 0; i < SB; ++i)
-            if (q0 + i < qe) ld_rec(car + (q0 + i) * qstride, R[i]);
+            if (q0 + i < qe) ld_rec(A, q0 + i, sys, R[i]);
 #pragma unroll
         for (int i = 0; i < SB; ++i)
             if (q0 + i < qe) {
@@ -413,7 +499,7 @@ __device__ void scan_group(const Args<T> &A, ScanSmem<T> &S, int g, int sw, int 
                 mv(m, y0, y1, t0, t1);
                 y0 = t0 + yf0;
                 y1 = t1 + yf1;
-                st_rec(car + q * qstride, R[i]);
+                st_rec(A, q, sys, R[i]);
             }
     }
     // ---- backward fold of my segment (high to low): c = Mb c + c_q, Pb = prod Mb
@@ -422,7 +508,7 @@ __device__ void scan_group(const Args<T> &A, ScanSmem<T> &S, int g, int sw, int 
         T R[SB][4];
 #pragma unroll
         for (int i = 0; i < SB; ++i)
-            if (q1 - 1 - i >= qa) ld_rec(car + (q1 - 1 - i) * qstride, R[i]);
+            if (q1 - 1 - i >= qa) ld_rec(A, q1 - 1 - i, sys, R[i]);
 #pragma unroll
         for (int i = 0; i < SB; ++i)
             if (q1 - 1 - i >= qa) {
@@ -451,7 +537,7 @@ __device__ void scan_group(const Args<T> &A, ScanSmem<T> &S, int g, int sw, int 
         T R[SB][4];
 #pragma unroll
         for (int i = 0; i < SB; ++i)
-            if (q1 - 1 - i >= qa) ld_rec(car + (q1 - 1 - i) * qstride, R[i]);
+            if (q1 - 1 - i >= qa) ld_rec(A, q1 - 1 - i, sys, R[i]);
 #pragma unroll
         for (int i = 0; i < SB; ++i)
             if (q1 - 1 - i >= qa) {
@@ -464,7 +550,7 @@ __device__ void scan_group(const Args<T> &A, ScanSmem<T> &S, int g, int sw, int 
                 mv(m, z0, z1, t0, t1);
                 z0 = t0 + cq0;
                 z1 = t1 + cq1;
-                st_rec(car + q * qstride, R[i]);
+                st_rec(A, q, sys, R[i]);
             }
     }
     if (PER && sw == 0) {
@@ -492,6 +578,109 @@ __device__ void scan_group(const Args<T> &A, ScanSmem<T> &S, int g, int sw, int 
     }
 }
 
+// ---------------------------------------------------------------- windowed mode
+// The chunk maps of the LHS decay: ||Mf_{q+L-1}..Mf_q|| and ||Mb_q..Mb_{q+L-1}||
+// < 1e-18 for every q at L = A.win (checked when the handle is factored), so
+//   yin_q = sum_{p<q} Mf_{q-1}..Mf_{p+1} yF_p   and   zin_q = sum_{p>q} Mb_{q+1}..Mb_{p-1} c_p
+// (c_p = zB_p + H_p yin_p) are exact in fp64 when truncated to p in [q-L, q+L]:
+// the recurrences of the scan, run over that window from zero inflow.
+// yF(p) / zB(p) are (lane-private) loaders of the records.
+template <typename T, typename YF, typename ZB>
+__device__ __forceinline__ void window_inflow(const Args<T> &A, int q, YF yF, ZB zB, T &y0, T &y1, T &z0, T &z1)
+{
+    const int L = A.win, nq = A.nq;
+    T ya = T(0), yb = T(0), cz[LMAX][2];
+#pragma unroll
+    for (int d = 0; d < 2 * LMAX; ++d) {
+        if (d < 2 * L) {
+            const int p = q - L + d;
+            if (p >= 0 && p < nq) {
+                T m[4], f0, f1, t0, t1;
+                ldm4(A.ct + (int64_t)p * 12, m);
+                yF(d, p, f0, f1);
+                mv(m, ya, yb, t0, t1);
+                ya = t0 + f0;
+                yb = t1 + f1;
+            }
+            if (d == L - 1) y0 = ya, y1 = yb;        // after chunk q-1: yin_q
+            if (d >= L) {                            // after chunk q+e: yin_{q+1+e} -> c_{q+1+e}
+                const int e = d - L, pp = q + 1 + e;
+                if (pp < nq) {
+                    T h[4], b0, b1, t0, t1;
+                    ldm4(A.ct + (int64_t)pp * 12 + 8, h);
+                    zB(e, pp, b0, b1);
+                    mv(h, ya, yb, t0, t1);
+                    cz[e][0] = b0 + t0;
+                    cz[e][1] = b1 + t1;
+                }
+            }
+        }
+    }
+    T za = T(0), zb = T(0);
+#pragma unroll
+    for (int e = LMAX - 1; e >= 0; --e) {
+        const int pp = q + 1 + e;
+        if (e < L && pp < nq) {
+            T m[4], t0, t1;
+            ldm4(A.ct + (int64_t)pp * 12 + 4, m);
+            mv(m, za, zb, t0, t1);
+            za = t0 + cz[e][0];
+            zb = t1 + cz[e][1];
+        }
+    }
+    z0 = za, z1 = zb;
+}
+
+// Windowed mode, cyclic: Navon's pair x_l / Sherman–Morrison
+// of system `sys` of group g from the records near both ends.
+template <typename T, int K>
+__device__ void window_xl(const Args<T> &A, int64_t sys)
+{
+    const int L = A.win, nq = A.nq;
+    auto ldy = [&](int, int p, T &a, T &b) { ld_pair(A.car + rec_off(p, 0, sys, A.nsys), a, b); };
+    auto ldz = [&](int, int p, T &a, T &b) { ld_pair(A.car + rec_off(p, 1, sys, A.nsys), a, b); };
+    // (x_0, x_1) of the non-cyclic solution = c_0 + Mb_0 zin_0 (yin_0 = 0, c_0 = zB_0)
+    T y0, y1, z0, z1;
+    window_inflow<T>(A, 0, ldy, ldz, y0, y1, z0, z1);
+    T m[4], t0, t1, c0, c1;
+    ldm4(A.ct + 4, m);
+    ldz(0, 0, c0, c1);
+    mv(m, z0, z1, t0, t1);
+    const T y1c = c0 + t0, y2c = c1 + t1;
+    // true g on the cyclic rows: zero-inflow g + response to the chunk's inflow
+    T gv[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+    for (int jx = 0; jx < 4; ++jx) {
+        if (A.srow[jx] < 0) continue;
+        const int qj = (int)(A.srow[jx] / Q);
+        T a0 = T(0), a1 = T(0);
+        for (int p = max(0, qj - L); p < qj; ++p) {
+            T mm[4], f0, f1, u0, u1;
+            ldm4(A.ct + (int64_t)p * 12, mm);
+            ldy(0, p, f0, f1);
+            mv(mm, a0, a1, u0, u1);
+            a0 = u0 + f0;
+            a1 = u1 + f1;
+        }
+        gv[jx] = __ldcg(A.spec + sys * 4 + jx) + A.rsp[jx * 2] * a0 + A.rsp[jx * 2 + 1] * a1;
+    }
+    const double *sc = A.scal;
+    T xl0, xl1;
+    if (K == 2) {
+        const T ym1 = gv[1], ym2 = gv[0] - T(sc[10]) * gv[1];
+        const T q0 = gv[2] - (T(sc[4]) * y1c + T(sc[5]) * ym2 + T(sc[6]) * ym1);
+        const T q1 = gv[3] - (T(sc[7]) * y1c + T(sc[8]) * y2c + T(sc[9]) * ym1);
+        xl0 = T(sc[0]) * q0 + T(sc[1]) * q1;
+        xl1 = T(sc[2]) * q0 + T(sc[3]) * q1;
+    } else {
+        xl0 = (y1c + T(sc[0]) * gv[0]) / T(sc[1]);
+        xl1 = T(0);
+    }
+    __stcg(A.xl + sys * 2 + 0, xl0);
+    __stcg(A.xl + sys * 2 + 1, xl1);
+    (void)nq;
+}
+
 // ---------------------------------------------------------------- the kernel
 template <typename T>
 struct Smem {
@@ -501,12 +690,32 @@ struct Smem {
     ScanSmem<T> scan;
 };
 
-template <typename T, int K, bool PER>
+// f of the 1D CH step, in place over the warp's own tile column (lane-private)
+template <typename T>
+__device__ __forceinline__ void ch1d_rhs(T *du, const T *halo, int kmax, int lane, T alpha)
+{
+    T um = halo[lane];
+    T nm = um * um * um - um;
+    T u0 = du[lane];
+    T n0 = u0 * u0 * u0 - u0;
+#pragma unroll 4
+    for (int k = 0; k < kmax; ++k) {
+        const T u1 = (k + 1 < kmax) ? du[(k + 1) * TW + lane] : halo[TW + lane];
+        const T n1 = u1 * u1 * u1 - u1;
+        du[k * TW + lane] = u0 + alpha * (nm - T(2) * n0 + n1);
+        nm = n0;
+        n0 = n1;
+        u0 = u1;
+    }
+}
+
+template <typename T, int K, bool PER, int MODE, int LAY>
 __global__ void __launch_bounds__(NTHREADS, 1) fs_kernel(const __grid_constant__ CUtensorMap tmap, const Args<T> A)
 {
     constexpr int NS = Cfg<T>::NS, TILE = Cfg<T>::TILE;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    Smem<T> &sm = *reinterpret_cast<Smem<T> *>(smem_raw);
+    // 1024-byte aligned: the 128B swizzle pattern of LAY_CONTIG tiles repeats per 1 KB
+    Smem<T> &sm = *reinterpret_cast<Smem<T> *>((((uintptr_t)smem_raw) + 1023) & ~(uintptr_t)1023);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int i = 0; i < NS; ++i) {
@@ -520,18 +729,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) fs_kernel(const __grid_constant__
     if (warp == NC) {
         // ---------------- producer: claim NC items at a time, one per consumer warp
         if (lane == 0) {
+            const unsigned epoch = ld_relaxed(A.tick + 3) + 1u;
+            const unsigned need = epoch * (unsigned)A.nq;   // P1 tiles of a group done by this launch (mod 2^32)
             const uint64_t pol1 = policy_evict_last(), pol2 = policy_evict_first();
-            int64_t c = atomicAdd(A.tick, 1u);
             for (int64_t k = 0;; ++k) {
+                const int64_t c = blockIdx.x + k * gridDim.x;   // this CTA's k-th claim (static)
                 const bool done = c >= A.nclaims;
-                const int64_t cn = done ? c : (int64_t)atomicAdd(A.tick, 1u);   // next claim, consumed one round later
                 Item it[NC];
-                unsigned fl[NC];
+                unsigned f1[NC], f2[NC];
+                bool nx[NC];
 #pragma unroll
                 for (int w = 0; w < NC; ++w) {
                     const int64_t i = c * NC + w;
-                    it[w] = (!done && i < A.items) ? decode(i, A.nq, A.G, A.D) : Item{0, 0, 0};
-                    fl[w] = (!done && i < A.items && it[w].p2) ? ld_relaxed(A.flag + it[w].g) : A.epoch;
+                    const bool live = !done && i < A.items;
+                    it[w] = live ? decode(i, A.nq, A.G, A.D) : Item{0, 0, 0};
+                    const bool p2 = live && it[w].p2;
+                    // windowed: all P1 tiles of the group (monotone counter), + the group's
+                    // x_l where the chunk carries a cyclic correction; else the group scan
+                    nx[w] = PER && (!A.win || (p2 && A.needxl[it[w].q]));
+                    f1[w] = (p2 && A.win) ? ld_relaxed(A.cnt + it[w].g) : need;
+                    f2[w] = (p2 && (!A.win || nx[w])) ? ld_relaxed(A.flag + it[w].g) : epoch;
                 }
 #pragma unroll
                 for (int w = 0; w < NC; ++w) {
@@ -545,9 +762,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fs_kernel(const __grid_constant__
                     }
                     const Item id = it[w];
                     if (id.p2) {
-                        // the group's scan must be complete before its inflows are copied
-                        if (fl[w] != A.epoch)
-                            while (ld_acquire(A.flag + id.g) != A.epoch) __nanosleep(64);
+                        // the records (and x_l) must be complete before they are copied
+                        if (f1[w] != need)
+                            while (ld_acquire(A.cnt + id.g) != need) __nanosleep(64);
+                        if (f2[w] != epoch)
+                            while (ld_acquire(A.flag + id.g) != epoch) __nanosleep(64);
                         fence_acquire();
                         fence_proxy_global();
                     }
@@ -558,24 +777,68 @@ __global__ void __launch_bounds__(NTHREADS, 1) fs_kernel(const __grid_constant__
                     T *slot = sm.slot[sl];
                     const uint32_t cb = up16((uint32_t)(kmax * (id.p2 ? COEF_STRIDE : REC) * sizeof(T)));
                     uint32_t bytes = TILE * sizeof(T) + cb;
-                    if (id.p2) bytes += Cfg<T>::INF * sizeof(T) + (PER ? Cfg<T>::XL * sizeof(T) : 0);
+                    // P2 inflow data: group scan -> (yin, zin) blocks; windowed -> the yF
+                    // blocks of chunks [q-L, q+L-1] and zB blocks of [q+1, q+L] in range
+                    int nblk = 0;
+                    if (id.p2) {
+                        if (A.win) {
+                            for (int d = 0; d < 2 * A.win; ++d) nblk += (id.q - A.win + d >= 0 && id.q - A.win + d < A.nq);
+                            for (int e = 0; e < A.win; ++e) nblk += (id.q + 1 + e < A.nq);
+                        } else {
+                            nblk = 2;
+                        }
+                        bytes += (uint32_t)(nblk * 2 * TW * sizeof(T)) + (nx[w] ? Cfg<T>::XL * sizeof(T) : 0);
+                    }
+                    if (MODE == MODE_CH1D) bytes += Cfg<T>::HALO * sizeof(T);
                     bar_expect_tx(&sm.full[sl], bytes);
                     const uint64_t pol = id.p2 ? pol2 : pol1;
-                    if (A.flat)
+                    if (LAY == LAY_CONTIG) {
+                        // Q / EB boxes of (EB rows x 32 systems), 128B-swizzled
+#pragma unroll
+                        for (int bx = 0; bx < Q / Sw<T>::EB; ++bx) {
+                            T *dst = slot + bx * TW * Sw<T>::EB;
+                            const int r = (int)r0 + bx * Sw<T>::EB;
+                            if (A.flat) tma_load2(dst, &tmap, r, (int)((int64_t)b * A.M + gl * TW), &sm.full[sl], pol);
+                            else tma_load3(dst, &tmap, r, gl * TW, b, &sm.full[sl], pol);
+                        }
+                    } else if (A.flat) {
                         tma_load2(slot, &tmap, gl * TW, (int)((int64_t)b * A.n + r0), &sm.full[sl], pol);
-                    else
+                    } else {
                         tma_load3(slot, &tmap, gl * TW, (int)r0, b, &sm.full[sl], pol);
+                    }
                     bulk_load(slot + TILE, id.p2 ? A.coef + r0 * COEF_STRIDE : A.rec + r0 * REC, cb, &sm.full[sl]);
+                    if (MODE == MODE_CH1D) {
+                        // the tile's periodic halo rows (32 contiguous systems each)
+                        const T *ub = A.x + (int64_t)b * A.bstride + (int64_t)gl * TW;
+                        const int64_t rlo = r0 == 0 ? A.n - 1 : r0 - 1, rhi = r0 + kmax == A.n ? 0 : r0 + kmax;
+                        T *hs = slot + TILE + Cfg<T>::COEF + Cfg<T>::INF + Cfg<T>::XL;
+                        bulk_load(hs, ub + rlo * A.pitch, TW * sizeof(T), &sm.full[sl]);
+                        bulk_load(hs + TW, ub + rhi * A.pitch, TW * sizeof(T), &sm.full[sl]);
+                    }
                     if (id.p2) {
-                        bulk_load(slot + TILE + Cfg<T>::COEF, A.car + ((int64_t)id.q * A.nsys + (int64_t)id.g * TW) * 4,
-                                  Cfg<T>::INF * sizeof(T), &sm.full[sl]);
-                        if (PER)
-                            bulk_load(slot + TILE + Cfg<T>::COEF + Cfg<T>::INF, A.xl + (int64_t)id.g * TW * 2,
-                                      Cfg<T>::XL * sizeof(T), &sm.full[sl]);
+                        T *ia = slot + TILE + Cfg<T>::COEF;
+                        const int64_t s0 = (int64_t)id.g * TW;
+                        constexpr uint32_t BB = 2 * TW * sizeof(T);   // one (q, half) block of the group
+                        if (A.win) {
+                            for (int d = 0; d < 2 * A.win; ++d) {
+                                const int p = id.q - A.win + d;
+                                if (p >= 0 && p < A.nq) bulk_load(ia + d * 2 * TW, A.car + rec_off(p, 0, s0, A.nsys), BB, &sm.full[sl]);
+                            }
+                            for (int e = 0; e < A.win; ++e) {
+                                const int p = id.q + 1 + e;
+                                if (p < A.nq)
+                                    bulk_load(ia + (2 * LMAX + e) * 2 * TW, A.car + rec_off(p, 1, s0, A.nsys), BB, &sm.full[sl]);
+                            }
+                        } else {
+                            bulk_load(ia, A.car + rec_off(id.q, 0, s0, A.nsys), BB, &sm.full[sl]);
+                            bulk_load(ia + 2 * TW, A.car + rec_off(id.q, 1, s0, A.nsys), BB, &sm.full[sl]);
+                        }
+                        if (nx[w])
+                            bulk_load(slot + TILE + Cfg<T>::COEF + Cfg<T>::INF, A.xl + s0 * 2, Cfg<T>::XL * sizeof(T),
+                                      &sm.full[sl]);
                     }
                 }
                 if (done) break;
-                c = cn;
             }
         }
     } else if (warp < NC) {
@@ -584,7 +847,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fs_kernel(const __grid_constant__
             const int sl = (int)(j % NS);
             bar_wait(&sm.full[sl], (uint32_t)((j / NS) & 1));
             const int64_t i = *(volatile int64_t *)&sm.item[sl];
-            if (i == -1) break;
+            if (i == -1) {
+                if (LAY == LAY_CONTIG && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+                break;
+            }
             if (i < 0) {
                 __syncwarp();
                 if (lane == 0) bar_arrive(&sm.empty[sl]);
@@ -599,6 +865,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fs_kernel(const __grid_constant__
             const int64_t s_in_batch = (int64_t)gl * TW + lane;
             const bool ok = s_in_batch < A.M;
             const int64_t sys = (int64_t)id.g * TW + lane;
+            if (MODE == MODE_CH1D)
+                ch1d_rhs<T>(const_cast<T *>(d), d + TILE + Cfg<T>::COEF + Cfg<T>::INF + Cfg<T>::XL, kmax, lane, A.alpha);
             if (!id.p2) {
                 if (PER && id.q >= A.qspec) {
                     int ks[4];
@@ -607,11 +875,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fs_kernel(const __grid_constant__
                         const int64_t rr = A.srow[jx] - r0;
                         ks[jx] = (A.srow[jx] >= 0 && rr >= 0 && rr < Q) ? (int)rr : -1;
                     }
-                    tile_carry<T, K, true, false>(d, c, kmax, lane, ks, A, sys, ok, id.q);
+                    tile_carry<T, K, true, false, LAY>(d, c, kmax, lane, ks, A, sys, ok, id.q);
                 } else {
                     const int ks[4] = {-1, -1, -1, -1};
-                    if (kmax == Q) tile_carry<T, K, false, true>(d, c, Q, lane, ks, A, sys, ok, id.q);
-                    else tile_carry<T, K, false, false>(d, c, kmax, lane, ks, A, sys, ok, id.q);
+                    if (kmax == Q) tile_carry<T, K, false, true, LAY>(d, c, Q, lane, ks, A, sys, ok, id.q);
+                    else tile_carry<T, K, false, false, LAY>(d, c, kmax, lane, ks, A, sys, ok, id.q);
                 }
                 __syncwarp();
                 if (lane == 0) bar_arrive(&sm.empty[sl]);
@@ -624,16 +892,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) fs_kernel(const __grid_constant__
             // P2: the column, inflows and x_l into registers
             T v[Q];
 #pragma unroll
-            for (int k = 0; k < Q; ++k) v[k] = d[k * TW + lane];
+            for (int k = 0; k < Q; ++k) v[k] = tld<T, LAY>(d, k, lane);
             const T *inf = c + Cfg<T>::COEF;
             T y0, y1, z0, z1, xl0 = T(0), xl1 = T(0);
-            lds2(inf + lane * 4, y0, y1);
-            lds2(inf + lane * 4 + 2, z0, z1);
-            if (PER) lds2(inf + Cfg<T>::INF + lane * 2, xl0, xl1);
+            if (A.win) {
+                auto ldy = [&](int d, int, T &a, T &bb) { lds2(inf + d * 2 * TW + lane * 2, a, bb); };
+                auto ldz = [&](int e, int, T &a, T &bb) { lds2(inf + (2 * LMAX + e) * 2 * TW + lane * 2, a, bb); };
+                window_inflow<T>(A, id.q, ldy, ldz, y0, y1, z0, z1);
+                if (PER && A.needxl[id.q]) lds2(inf + Cfg<T>::INF + lane * 2, xl0, xl1);
+            } else {
+                lds2(inf + lane * 2, y0, y1);
+                lds2(inf + 2 * TW + lane * 2, z0, z1);
+                if (PER) lds2(inf + Cfg<T>::INF + lane * 2, xl0, xl1);
+            }
             if (kmax == Q) tile_solve<T, K, PER, true>(v, c, Q, y0, y1, z0, z1, xl0, xl1);
             else tile_solve<T, K, PER, false>(v, c, kmax, y0, y1, z0, z1, xl0, xl1);
-            __syncwarp();
-            if (lane == 0) bar_arrive(&sm.empty[sl]);
             if (PER && K == 2 && r0 + Q > A.n - 2) {
                 // Navon: the last two unknowns are x_l itself
                 const int k2 = (int)(A.n - 2 - r0);
@@ -643,12 +916,38 @@ __global__ void __launch_bounds__(NTHREADS, 1) fs_kernel(const __grid_constant__
                     if (k == k2 + 1) v[k] = xl1;
                 }
             }
+            if (LAY == LAY_CONTIG) {
+                // x back into the slot (same swizzle) and out by TMA: systems are
+                // rows of the output, so a register store would scatter 32 lines
+                T *dm = const_cast<T *>(d);
+#pragma unroll
+                for (int k = 0; k < Q; ++k) tst<T, LAY>(dm, k, lane, v[k]);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+#pragma unroll
+                    for (int bx = 0; bx < Q / Sw<T>::EB; ++bx) {
+                        const int r = (int)r0 + bx * Sw<T>::EB;
+                        if (r < A.n) {
+                            if (A.flat) tma_store2(&tmap, r, (int)((int64_t)b * A.M + gl * TW), dm + bx * TW * Sw<T>::EB);
+                            else tma_store3(&tmap, r, gl * TW, b, dm + bx * TW * Sw<T>::EB);
+                        }
+                    }
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // slot read out: reusable
+                    bar_arrive(&sm.empty[sl]);
+                }
+                __syncwarp();
+                continue;
+            }
+            __syncwarp();
+            if (lane == 0) bar_arrive(&sm.empty[sl]);
             if (ok) {
                 // x in place: every row of the tile is one contiguous 32-system segment
                 // (opaque stride: one running address instead of Q live ones)
-                int64_t Mo = A.M;
+                int64_t Mo = A.pitch;
                 asm volatile("" : "+l"(Mo));
-                T *x = A.x + (int64_t)b * A.bstride + r0 * Mo + s_in_batch;
+                T *x = A.xout + (int64_t)b * A.bstride + r0 * Mo + s_in_batch;
 #pragma unroll
                 for (int k = 0; k < Q; ++k) {
                     if (kmax == Q || k < kmax) __stcs(x, v[k]);
@@ -659,19 +958,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) fs_kernel(const __grid_constant__
     } else {
         // ---------------- scan team: groups claimed in order, each after its P1 tiles
         const int sw = warp - NC - 1;
-        for (;;) {
-            if (sw == 0 && lane == 0) sm.scan.grp = (int)atomicAdd(A.tick + 1, 1u);
-            scan_bar();
-            const int g = sm.scan.grp;
-            if (g >= A.G) break;
-            while (ld_acquire(A.cnt + g) < (unsigned)A.nq) __nanosleep(128);
-            scan_group<T, K, PER>(A, sm.scan, g, sw, lane);
-            __threadfence();
-            fence_proxy_global();
-            scan_bar();   // all records / x_l of the group written (and sm.scan.grp consumed)
-            if (sw == 0 && lane == 0) {
-                A.cnt[g] = 0u;
-                st_release(A.flag + g, A.epoch);
+        const unsigned epoch = ld_relaxed(A.tick + 3) + 1u;
+        const unsigned need = epoch * (unsigned)A.nq;
+        if (A.win) {
+            // windowed: no scan; cyclic systems get x_l per group from the end records
+            if (PER && sw == 0) {
+                for (int g = blockIdx.x; g < A.G; g += gridDim.x) {   // groups in order (static)
+                    while (ld_acquire(A.cnt + g) != need) __nanosleep(128);
+                    window_xl<T, K>(A, (int64_t)g * TW + lane);
+                    __threadfence();
+                    fence_proxy_global();
+                    __syncwarp();
+                    if (lane == 0) st_release(A.flag + g, epoch);
+                }
+            }
+        } else {
+            for (int g = blockIdx.x; g < A.G; g += gridDim.x) {   // groups in order (static)
+                while (ld_acquire(A.cnt + g) != need) __nanosleep(128);
+                scan_group<T, K, PER>(A, sm.scan, g, sw, lane);
+                __threadfence();
+                fence_proxy_global();
+                scan_bar();   // all records / x_l of the group written
+                if (sw == 0 && lane == 0) st_release(A.flag + g, epoch);
             }
         }
     }
@@ -680,9 +988,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fs_kernel(const __grid_constant__
     if (threadIdx.x == 0) {
         __threadfence();
         if (atomicAdd(A.tick + 2, 1u) == gridDim.x - 1) {
-            A.tick[0] = 0u;
-            A.tick[1] = 0u;
             A.tick[2] = 0u;
+            A.tick[3] = A.tick[3] + 1u;   // every CTA has read this launch's epoch
             __threadfence();
         }
     }

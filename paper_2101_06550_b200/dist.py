@@ -75,10 +75,12 @@ class RankState:
         self.cm = torch.zeros((r + 4, n), dtype=dt, device=dev)
         self.cn[2:r + 2] = cn_rows
         self.cm[2:r + 2] = cm_rows
-        self.w = torch.empty((r, n), dtype=dt, device=dev)
-        self.packed = torch.empty((P, r, n // P), dtype=dt, device=dev)
-        self.cols = torch.empty((P, r, n // P), dtype=dt, device=dev)   # = [n][n/P] column block
-        self.back = torch.empty((P, r, n // P), dtype=dt, device=dev)
+        # the sweep intermediates are fp64 for either state dtype (pentab.h ch_dist_pass_a)
+        f64 = torch.float64
+        self.w = torch.empty((r, n), dtype=f64, device=dev)
+        self.packed = torch.empty((P, r, n // P), dtype=f64, device=dev)
+        self.cols = torch.empty((P, r, n // P), dtype=f64, device=dev)   # = [n][n/P] column block
+        self.back = torch.empty((P, r, n // P), dtype=f64, device=dev)
 
     def interior(self, which="cn"):
         r = self.prm.rows

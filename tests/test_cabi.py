@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "pentab.h")).read()
-    return set(re.findall(r"^PB_API\s+[a-z0-9_]+\s+\**([a-z_]+)\(", src, flags=re.M))
+    return set(re.findall(r"^PB_API\s+[a-z0-9_]+\s+\**([a-z0-9_]+)\(", src, flags=re.M))
 
 
 def test_header_and_binding_agree():

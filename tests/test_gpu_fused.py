@@ -153,3 +153,93 @@ def test_shape_changes_reuse_scratch():
             h.solve_many(x, cnt, n * 96)
         torch.cuda.synchronize()
         assert relerr(x.cpu().numpy(), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("case", ["pitched_inter", "pitched_contig", "grids_ysweep", "odd_strides"])
+def test_solve_strided(case, dtype):
+    """pent_solve_strided (pentab.h): pitched sub-blocks, batched
+    grids and arbitrary strides, against the oracle; elements outside the
+    addressed systems are untouched."""
+    n = 200
+    a, b, c, d, e = synth.dd_penta(n, 1, seed=61)
+    rng = synth.rng(62)
+    if case == "pitched_inter":        # systems [s0, s0+m) of an interleaved array with row pitch P
+        P, s0, m, cnt = 100, 12, 40, 1
+        buf = rng.uniform(-1, 1, size=n * P)
+        lay = dict(n_inner=m, inner_stride=1, n_outer=1, outer_stride=0, row_stride=P, offset=s0)
+        idx = lambda bb, s, i: s0 + s + i * P
+    elif case == "pitched_contig":     # rows of pitch P >= n, two batches
+        P, m, cnt = 216, 37, 2
+        buf = rng.uniform(-1, 1, size=cnt * m * P + 8)
+        lay = dict(n_inner=m, inner_stride=P, n_outer=cnt, outer_stride=m * P + 8, row_stride=1, offset=0)
+        idx = lambda bb, s, i: bb * (m * P + 8) + s * P + i
+    elif case == "grids_ysweep":       # S grids n x n, systems = columns (the ADI y-sweep)
+        m, cnt = n, 3
+        buf = rng.uniform(-1, 1, size=cnt * n * n)
+        lay = dict(n_inner=n, inner_stride=1, n_outer=cnt, outer_stride=n * n, row_stride=n, offset=0)
+        idx = lambda bb, s, i: bb * n * n + s + i * n
+    else:                              # every other element, rows 2*m apart (thread-per-system path)
+        m, cnt = 30, 1
+        buf = rng.uniform(-1, 1, size=2 * m * n)
+        lay = dict(n_inner=m, inner_stride=2, n_outer=1, outer_stride=0, row_stride=2 * m, offset=0)
+        idx = lambda bb, s, i: 2 * s + i * 2 * m
+    if dtype == "f32":
+        buf = buf.astype(np.float32).astype(np.float64)
+    h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in (a, b, c, d, e)], batch=m, n=n, periodic=True,
+                       dtype=dtype)
+    x = torch.from_numpy(buf).to(TDT[dtype]).cuda()
+    h.solve_strided(x, **lay)
+    torch.cuda.synchronize()
+    got = x.double().cpu().numpy()
+    touched = np.zeros(buf.size, dtype=bool)
+    for bb in range(cnt):
+        ii = np.array([[idx(bb, s, i) for s in range(m)] for i in range(n)])   # [n][m]
+        touched[ii.reshape(-1)] = True
+        f = buf[ii].reshape(-1)
+        ref = oracle.penta_batch_solve(a, b, c, d, e, f, n=n, m=m, periodic=True)
+        assert relerr(got[ii].reshape(-1), ref) <= TOL[dtype], bb
+    assert np.array_equal(got[~touched], buf[~touched])
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_buffer_pipelined(pinned):
+    """A host right-hand side (>= 4096 systems) takes the pipelined path: pitched
+    H2D / fused solve / D2H of column blocks on two streams; sampled systems match
+    the oracle and the call returns with the host buffer solved."""
+    n, m = 300, 8192 + 96
+    a, b, c, d, e = synth.dd_penta(n, 1, seed=71)
+    f = synth.rhs_uniform(n, m, seed=72)
+    h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in (a, b, c, d, e)], batch=m, n=n, periodic=True)
+    x = torch.from_numpy(f.copy())
+    if pinned:
+        x = x.pin_memory()
+    h.solve(x.numpy())
+    X = x.numpy().reshape(n, m)
+    F = f.reshape(n, m)
+    for s in (0, 31, 4000, m - 1):
+        ref = oracle.penta_batch_solve(a, b, c, d, e, np.ascontiguousarray(F[:, s]), n=n, m=1, periodic=True)
+        assert relerr(X[:, s], ref) <= 1e-12, s
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("sigma,n,expect", [(45.09, 3000, "window"), (68.0, 700, "window"), (2700.0, 2000, "scan"),
+                                            (2700.0, 130, "scan")])
+def test_window_and_scan_modes(sigma, n, expect, dtype):
+    """Both inflow modes of the fused solve against the oracle: the thesis
+    operators at dx = 2 pi/256 (sigma 45-68) decay below 1e-18 within 3 chunks
+    (windowed inflows); sigma = 2700 (Table 3.1's n = 1024 at L = 2 pi) does
+    not (per-group scan).  Cyclic (Navon), several groups, ragged n."""
+    m = 200
+    diags = synth.const_penta(n, sigma, -4 * sigma, 1 + 6 * sigma, -4 * sigma, sigma)
+    f = synth.rhs_uniform(n, m, seed=n)
+    ref = oracle.penta_batch_solve(*diags, f, n=n, m=m, periodic=True)
+    h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in diags], batch=m, n=n, periodic=True, dtype=dtype)
+    w = h.window()
+    assert (w > 0) == (expect == "window"), w
+    x = torch.from_numpy(f).to(TDT[dtype]).cuda()
+    h.solve(x)
+    torch.cuda.synchronize()
+    # kappa = 1 + 16 sigma = 4.3e4 at sigma 2700: fp32 is kappa-limited there (SURVEY §8(c): ~1.7e-4 measured)
+    tol = TOL[dtype] if sigma < 100 else (1e-12 if dtype == "f64" else 1e-3)
+    assert relerr(x.double().cpu().numpy(), ref) <= tol

@@ -90,18 +90,18 @@ def test_adi_parity_fp64(n, sims, L):
 
 @pytest.mark.parametrize("n", [64, 256, 512])
 def test_adi_parity_fp32(n):
-    """fp32 vs the fp64 oracle.  The explicit term k_bih*BIH(Cbar) has weights
-    summing to 64 sigma in magnitude (sigma = 45.09), so each step carries an
-    fp32 rounding of ~eps32 (1 + 64 sigma) max|Cbar|: bound 3 steps x
-    eps32 x (1 + 64 sigma) = 5.2e-4 relative."""
+    """fp32 state vs the fp64 oracle at the north-star bar (<= 1e-5), 3 steps.
+    The RHS and both sweeps run on an fp64 workspace (reading r22: the explicit
+    biharmonic term is ~64 sigma |C| before the sweeps cancel it), so only the
+    stored levels round to fp32."""
     L = n * synth.DX_STATS
     dt = synth.ch_dt(n, L)
-    c0 = synth.ch_ic_random(2, n, seed=4)
+    c0 = synth.ch_ic_random(2, n, seed=4).astype(np.float32).astype(np.float64)
     rn, _ = oracle.ch_adi_steps(c0, c0, 3, dt=dt, D=1.0, gamma=0.01, L=L)
     gn, _ = gpu_adi(c0, 3, dt=dt, L=L, dtype="f32")
     err = relerr(gn, rn)
     print(f"ADI fp32 n={n} relerr {err:.2e}")
-    assert err <= 3 * 5.96e-8 * (1 + 64 * synth.SIGMA_STATS)
+    assert err <= 1e-5
 
 
 def test_adi_mass_conservation_and_fixed_point():
