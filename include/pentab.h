@@ -135,13 +135,12 @@ typedef struct {
 } pb_layout;
 PB_API int pent_solve_strided(pb_penta_t h, void *rhs, const pb_layout *L, void *stream);
 
-/* pent_solve_info — how the handle's shared-LHS solve resolves the chunk
- * inflows of the fused streaming solve (diagnostic): *window = L > 0 when the
- * chunk maps of the factored LHS decay below 1e-18 within L 64-row chunks
- * (each chunk's inflows then come from its 2L+1 neighbours), 0 when a full
- * per-group scan is used, -1 when the handle has no fused plan (per-system
- * LHS or N too large).                                                      */
-PB_API int pent_solve_info(pb_penta_t h, int *window);
+/* pent_solve_info — diagnostic: the configuration of the fused streaming
+ * solve for one batch of the handle in `layout`: info[0] = thread-block
+ * cluster size CS (0 = N beyond the cluster span, the global-scan kernel
+ * serves), info[1] = 64-row chunks per CTA, info[2] = clusters launched;
+ * all -1 when the handle has no fused plan (per-system LHS).               */
+PB_API int pent_solve_info(pb_penta_t h, int layout, int *info);
 
 PB_API int pent_destroy(pb_penta_t h);
 

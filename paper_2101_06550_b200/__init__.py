@@ -80,7 +80,7 @@ def lib() -> ctypes.CDLL:
         L.pent_solve_many.argtypes = [P, P, I, I64, I64, P]
         L.pent_solve_strided.argtypes = [P, P, ctypes.POINTER(pb_layout), P]
         L.tri_solve_strided.argtypes = [P, P, ctypes.POINTER(pb_layout), P]
-        L.pent_solve_info.argtypes = [P, ctypes.POINTER(ctypes.c_int)]
+        L.pent_solve_info.argtypes = [P, I, ctypes.POINTER(ctypes.c_int)]
         L.pent_destroy.argtypes = [P]
         L.tri_factor.argtypes = [I64, I64, P, P, P, I64, I, I, P, ctypes.POINTER(P)]
         L.tri_solve.argtypes = [P, P, I, P]
@@ -181,11 +181,12 @@ class PentaHandle(_Banded):
         _check(lib().pent_solve(self._h, _ptr(rhs), _layout(layout), _stream(rhs, stream)))
         return rhs
 
-    def window(self):
-        """pent_solve_info: chunk window of the fused solve (0 = group scan, -1 = none)."""
-        w = ctypes.c_int()
-        _check(lib().pent_solve_info(self._h, ctypes.byref(w)))
-        return w.value
+    def solve_info(self, layout="interleaved"):
+        """pent_solve_info: (cluster size, chunks per CTA, clusters) of the fused
+        solve; cluster size 0 = global-scan kernel, -1 = no fused plan."""
+        w = (ctypes.c_int * 3)()
+        _check(lib().pent_solve_info(self._h, _layout(layout), w))
+        return tuple(w)
 
     def solve_many(self, rhs, count, batch_stride, layout="interleaved", stream=None):
         _check(lib().pent_solve_many(self._h, _ptr(rhs), _layout(layout), count, batch_stride, _stream(rhs, stream)))

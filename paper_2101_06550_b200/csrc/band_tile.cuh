@@ -31,11 +31,10 @@ struct FusedScratch {
 };
 struct FusedPlan {
     int ok = 0, nq = 0;
-    int win = 0;                        // windowed inflows over 2*win+1 chunks (0: group scan)
-    unsigned char *needxl = nullptr;    // [nq] chunk carries a cyclic correction (device)
     void *rec = nullptr, *ct = nullptr, *rsp = nullptr;
     mutable std::mutex mu;
     mutable std::map<cudaStream_t, FusedScratch> scratch;
+    mutable cudaStream_t pipe[2] = {nullptr, nullptr};   // internal streams of the host-buffer pipeline
 };
 
 struct Band {
@@ -67,11 +66,10 @@ struct Band {
         cudaFree(fplan.rec);
         cudaFree(fplan.ct);
         cudaFree(fplan.rsp);
-        cudaFree(fplan.needxl);
-        for (auto &kv : fplan.scratch) {
-            cudaStreamSynchronize(kv.first);
-            cudaFree(kv.second.buf);
-        }
+        if (!fplan.scratch.empty() || fplan.pipe[0]) cudaDeviceSynchronize();   // queued solves may use the scratch
+        for (auto &kv : fplan.scratch) cudaFree(kv.second.buf);
+        for (auto s : fplan.pipe)
+            if (s) cudaStreamDestroy(s);
     }
 };
 
@@ -225,9 +223,9 @@ static int launch_tile_l(const Band *h, T *x, int layout, int64_t count, int64_t
 int const_penta_band(int64_t n, double sigma, int dtype, int cfg, int C, cudaStream_t st, Band **out);
 
 int fused_build_tables(Band *h, cudaStream_t st);
-// after the factor's sync: choose windowed or group-scan inflows from the decay
-// of the chunk maps, and mark the chunks that carry a cyclic correction
-int fused_window_plan(Band *h);
+// the cluster configuration {CS, cpc, clusters} of a fused solve of M x count systems
+// (CS = 0: the global-scan kernel serves)
+int fused_info(const Band *h, int layout, int64_t M, int64_t count, int *info);
 // the dispatching solves behind pent_solve / pent_solve_many / pent_solve_strided / tri_*
 int band_solve(const Band *h, void *rhs, int layout, int64_t count, int64_t bstride, cudaStream_t st);
 int band_solve_layout(const Band *h, void *rhs, const pb_layout &L, cudaStream_t st);

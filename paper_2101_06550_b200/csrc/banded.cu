@@ -586,7 +586,6 @@ static int factor_impl(Band *h, const double *a, const double *b, const double *
         set_pivot(sys, -1);
         return code;
     }
-    if (h->shared()) return fused_window_plan(h);
     return PB_OK;
 }
 
@@ -615,12 +614,17 @@ static int pipelined_host_solve(const Band *h, void *host, const pb_layout &L, c
                 if (buf[k]) cudaFreeAsync(buf[k], owner);
             for (auto ev : e)
                 if (ev) cudaEventDestroy(ev);
-            for (auto x : s)
-                if (x) cudaStreamDestroy(x);
         }
     } R;
     R.owner = st;
-    for (int k = 0; k < 2; ++k) PB_CUDA_TRY(cudaStreamCreateWithFlags(&R.s[k], cudaStreamNonBlocking));
+    {
+        // the handle's two pipeline streams (created once; their scratch is reused)
+        std::lock_guard<std::mutex> lk(h->fplan.mu);
+        for (int k = 0; k < 2; ++k)
+            if (!h->fplan.pipe[k]) PB_CUDA_TRY(cudaStreamCreateWithFlags(&h->fplan.pipe[k], cudaStreamNonBlocking));
+        R.s[0] = h->fplan.pipe[0];
+        R.s[1] = h->fplan.pipe[1];
+    }
     for (int k = 0; k < 3; ++k) PB_CUDA_TRY(cudaEventCreateWithFlags(&R.e[k], cudaEventDisableTiming));
     const size_t cbytes = es * (size_t)mc * (size_t)n;
     for (int k = 0; k < 2; ++k) PB_CUDA_TRY(cudaMallocAsync(&R.buf[k], cbytes, st));
@@ -804,11 +808,13 @@ int pent_solve_strided(pb_penta_t h, void *rhs, const pb_layout *L, void *stream
     return pb::band_solve_layout(h, rhs, *L, (cudaStream_t)stream);
 }
 
-int pent_solve_info(pb_penta_t h, int *window)
+int pent_solve_info(pb_penta_t h, int layout, int *info)
 {
-    if (!h || !window) return pb::set_error(PB_EINVAL, "null argument");
-    *window = (h->shared() && h->fplan.ok) ? h->fplan.win : -1;
-    return PB_OK;
+    if (!h || !info || (layout != PB_INTERLEAVED && layout != PB_CONTIGUOUS))
+        return pb::set_error(PB_EINVAL, "bad argument");
+    info[0] = info[1] = info[2] = -1;
+    if (!h->shared() || !h->fplan.ok) return PB_OK;
+    return pb::fused_info(h, layout, h->batch, 1, info);
 }
 
 int pent_destroy(pb_penta_t h)

@@ -1,0 +1,376 @@
+// fused_part.cuh — launchers of the fused solve kernels (fused_cluster.cuh,
+// fused_solve.cuh) for one (dtype, layout); included by fused_part_*.cu with
+// FS_T / FS_LAY / FS_NAME defined, so the instantiations compile in parallel.
+#include <cudaTypedefs.h>
+#include <math.h>
+#include <string.h>
+
+#include "band_tile.cuh"
+#include "fused_cluster.cuh"
+
+namespace pb {
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
+int fs_sm_count();
+
+// L2 budget for the lag window of f between P1(g) and P2(g) (the L2 is 126 MB;
+// the window, the x write-back in flight and the scratch records share it)
+constexpr double FS_L2_BUDGET = 40.0 * 1048576.0;   // lag window of f between P1(g) and P2(g)
+
+// Tensor map over x for either layout, cached per (stream, layout).
+// Interleaved: dims (M, n, count), box (32 systems, 64 rows, 1); contiguous:
+// dims (n, M, count), box (128 B of rows, 32 systems, 1), 128B swizzle.  OOB
+// loads zero-fill and OOB stores are clipped (ragged M and n).  Batches that
+// tiles cannot straddle use one 2-D view (flat).
+template <typename T, int LAY>
+static int tensor_map_for(FusedScratch &S, T *x, int64_t M, int64_t n, int64_t count, int64_t bstride, int64_t P,
+                          CUtensorMap *out, bool *flat_out)
+{
+    const int64_t dpitch = LAY == fs::LAY_CONTIG ? n : M;
+    const bool flat = P == dpitch && (LAY == fs::LAY_CONTIG
+                          ? (count == 1 || (bstride == M * n && M % fs::TW == 0))
+                          : (count == 1 || (bstride == M * n && n % fs::Q == 0 && n * count < ((int64_t)1 << 31))));
+    const uint64_t key[6] = {(uint64_t)(uintptr_t)x, (uint64_t)M, (uint64_t)n, (uint64_t)count, (uint64_t)bstride,
+                             (uint64_t)P * 16 + sizeof(T) * 2 + LAY};
+    uint64_t *skey = S.key[LAY];
+    void *smap = S.tmap[LAY];
+    if (memcmp(key, skey, sizeof(key)) != 0) {
+        auto enc = tensor_map_encoder();
+        if (!enc) return set_error(PB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        const auto dt = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+        const int rank = flat ? 2 : 3;
+        const int64_t bs = count > 1 ? bstride : P * (LAY == fs::LAY_CONTIG ? M : n);
+        CUresult r;
+        cuuint32_t estr[3] = {1, 1, 1};
+        if (LAY == fs::LAY_CONTIG) {
+            cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)(flat ? M * count : M), (cuuint64_t)(flat ? 1 : count)};
+            cuuint64_t strides[2] = {(cuuint64_t)(P * sizeof(T)), (cuuint64_t)(bs * sizeof(T))};
+            cuuint32_t box[3] = {(cuuint32_t)fs::Sw<T>::EB, (cuuint32_t)fs::TW, 1};
+            r = enc((CUtensorMap *)smap, dt, rank, (void *)x, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        } else {
+            cuuint64_t dims[3] = {(cuuint64_t)M, (cuuint64_t)(flat ? n * count : n), (cuuint64_t)(flat ? 1 : count)};
+            cuuint64_t strides[2] = {(cuuint64_t)(P * sizeof(T)), (cuuint64_t)(bs * sizeof(T))};
+            cuuint32_t box[3] = {(cuuint32_t)fs::TW, (cuuint32_t)fs::Q, 1};
+            r = enc((CUtensorMap *)smap, dt, rank, (void *)x, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        }
+        if (r != CUDA_SUCCESS) return set_error(PB_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+        memcpy(skey, key, sizeof(key));
+    }
+    memcpy(out, smap, sizeof(CUtensorMap));
+    *flat_out = flat;
+    return PB_OK;
+}
+
+// ---------------------------------------------------------------- cluster kernel launcher
+// Cluster size CS and chunks per CTA cpc = ceil(nq / CS) <= CPC: the candidate
+// that keeps the most SMs busy over the batch's groups (waves of NCL clusters,
+// NCL from the occupancy API), preferring cpc >= 4 and then the smaller CS.
+// Returns PB_EUNSUPPORTED when no cluster size fits (the global kernel serves).
+template <typename T, int K, bool PER, int MODE, int LAY>
+static int fc_launch_t(const Band *h, T *x, T *xout, double alpha, int64_t count, int64_t bstride, cudaStream_t st,
+                       int64_t Mo, int64_t pitch, int *info = nullptr)
+{
+    using C = fc::CCfg<T>;
+    auto kern = fc::fc_kernel<T, K, PER, MODE, LAY>;
+    const size_t smem = sizeof(fc::CSmem<T>) + 1024;
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    static int ncl_of[fc::CSMAX + 1];
+    std::call_once(once, [&] {
+        attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (attr == cudaSuccess) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaGetLastError();
+        for (int cs = 1; cs <= fc::CSMAX; cs *= 2) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)(cs * 16));
+            cfg.blockDim = dim3(fc::NTHREADS);
+            cfg.dynamicSmemBytes = smem;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = cs;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int ncl = 0;
+            if (attr == cudaSuccess && cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess) ncl = 0;
+            cudaGetLastError();
+            ncl_of[cs] = ncl;
+        }
+    });
+    if (attr != cudaSuccess) return set_error(PB_ECUDA, "fc_kernel smem attribute: %s", cudaGetErrorString(attr));
+    const int64_t M = Mo > 0 ? Mo : h->batch, n = h->n;
+    const int64_t P = pitch > 0 ? pitch : (LAY == fs::LAY_CONTIG ? n : M);
+    const int nq = h->fplan.nq;
+    const int64_t Gb = (M + fs::TW - 1) / fs::TW, G = Gb * count;
+    if (G > (1 << 30)) return PB_EUNSUPPORTED;
+    const int nsm = fs_sm_count();
+    int best_cs = 0, best_cpc = 0, best_ncl = 0;
+    double best = -1;
+    for (int cs = 1; cs <= fc::CSMAX; cs *= 2) {
+        const int cpc = (nq + cs - 1) / cs;
+        if (cpc > C::CPC || ncl_of[cs] < 1 || (cs > 1 && cpc * (cs - 1) >= nq)) continue;   // (every CTA owns chunks)
+        const int64_t ncl = std::min<int64_t>(ncl_of[cs], G);
+        const int64_t waves = (G + ncl - 1) / ncl;
+        double eff = (double)G / (double)(waves * ncl) * (double)(ncl * cs) / (double)nsm;
+        if (cpc < 4 && nq >= 4) eff *= 0.85;
+        if (eff > best * 1.01) {
+            best = eff;
+            best_cs = cs;
+            best_cpc = cpc;
+            best_ncl = (int)ncl;
+        }
+    }
+    if (info) {
+        info[0] = best_cs;
+        info[1] = best_cpc;
+        info[2] = best_ncl;
+        return PB_OK;
+    }
+    if (!best_cs) return PB_EUNSUPPORTED;
+
+    fc::CArgs<T> A;
+    CUtensorMap tmap;
+    {
+        std::lock_guard<std::mutex> lk(h->fplan.mu);
+        FusedScratch &S = h->fplan.scratch[st];
+        bool flat = false;
+        int rc = tensor_map_for<T, LAY>(S, x, M, n, count, bstride, P, &tmap, &flat);
+        if (rc) return rc;
+        A.flat = flat ? 1 : 0;
+    }
+    A.rec = (const T *)h->fplan.rec;
+    A.coef = (const T *)h->coef;
+    A.ct = (const T *)h->fplan.ct;
+    A.rsp = (const T *)h->fplan.rsp;
+    A.scal = h->scal;
+    A.x = x;
+    A.xout = xout;
+    A.alpha = (T)alpha;
+    A.n = n;
+    A.M = M;
+    A.bstride = count > 1 ? bstride : P * (LAY == fs::LAY_CONTIG ? M : n);
+    A.pitch = P;
+    for (int j = 0; j < 4; ++j) A.srow[j] = h->srow[j];
+    A.nq = nq;
+    A.count = (int)count;
+    A.Gb = (int)Gb;
+    A.G = (int)G;
+    A.cs = best_cs;
+    A.cpc = best_cpc;
+    A.ncl = best_ncl;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(best_ncl * best_cs));
+    cfg.blockDim = dim3(fc::NTHREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = best_cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    PB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tmap, A));
+    PB_LAUNCH_CHECK();
+    return PB_OK;
+}
+
+template <typename T, int K, bool PER, int MODE, int LAY>
+static int fs_launch_t(const Band *h, T *x, T *xout, double alpha, int64_t count, int64_t bstride, cudaStream_t st,
+                       int64_t Mo, int64_t pitch)
+{
+    auto kern = fs::fs_kernel<T, K, PER, MODE, LAY>;
+    const size_t smem = sizeof(fs::Smem<T>) + 1024;   // + alignment to 1 KB
+    static std::once_flag attr_once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once, [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    if (attr_err != cudaSuccess) return set_error(PB_ECUDA, "fs_kernel smem attribute: %s", cudaGetErrorString(attr_err));
+
+    const int64_t M = Mo > 0 ? Mo : h->batch, n = h->n;
+    const int64_t dpitch = LAY == fs::LAY_CONTIG ? n : M;   // the packed pitch
+    const int64_t P = pitch > 0 ? pitch : dpitch;
+    const int nq = h->fplan.nq;
+    const int64_t Gb = (M + fs::TW - 1) / fs::TW, G = Gb * count;
+    if (G > INT32_MAX / 2) return set_error(PB_EINVAL, "too many systems for one launch");
+    const int64_t nsys = G * fs::TW;
+    const int64_t items = 2 * G * nq, nclaims = (items + fs::NC - 1) / fs::NC;
+    const size_t es = sizeof(T);
+    // scratch: car [nq][nsys][4], spec [nsys][4], xl [nsys][2], cnt [G], flag [G], tick [4]
+    // (tick[2] CTAs done, tick[3] launches done)
+    const size_t off_spec = es * (size_t)nq * nsys * 4, off_xl = off_spec + es * nsys * 4;
+    const size_t off_cnt = (off_xl + es * nsys * 2 + 255) / 256 * 256;
+    const size_t off_flag = off_cnt + 4 * (size_t)G, off_tick = off_flag + 4 * (size_t)G;
+    const size_t need = off_tick + 16;   // tick[4]
+
+    fs::Args<T> A;
+    {
+        std::lock_guard<std::mutex> lk(h->fplan.mu);
+        FusedScratch &S = h->fplan.scratch[st];
+        if (need > S.bytes) {
+            if (S.buf) {
+                PB_CUDA_TRY(cudaStreamSynchronize(st));   // queued solves may still use the old scratch
+                cudaFree(S.buf);
+                S.buf = nullptr;
+                S.bytes = 0;
+            }
+            PB_CUDA_TRY(cudaMalloc(&S.buf, need));
+            S.bytes = need;
+            S.nq = S.nsys = -1;
+            memset(S.key, 0, sizeof(S.key));
+        }
+        char *base = (char *)S.buf;
+        if (S.nq != nq || S.nsys != nsys) {
+            // fresh scratch or new shape (the counters live at shape-dependent
+            // offsets): clear counters, flags and tickets; epochs restart at 1
+            PB_CUDA_TRY(cudaMemsetAsync(base + off_cnt, 0, need - off_cnt, st));
+            S.nq = nq;
+            S.nsys = nsys;
+        }
+        A.car = (T *)base;
+        A.spec = (T *)(base + off_spec);
+        A.xl = (T *)(base + off_xl);
+        A.cnt = (unsigned *)(base + off_cnt);
+        A.flag = (unsigned *)(base + off_flag);
+        A.tick = (unsigned *)(base + off_tick);
+
+        // tensor map over x, cached per stream.  Interleaved: dims (M, n, count),
+        // box (32 systems, 64 rows, 1); contiguous: dims (n, M, count), box
+        // (128 B of rows, 32 systems, 1), 128B swizzle.  OOB loads zero-fill and
+        // OOB stores are clipped (ragged M and n).  Contiguous batches that tiles
+        // cannot straddle use one 2-D view.
+        const bool flat = P == dpitch && (LAY == fs::LAY_CONTIG
+                              ? (count == 1 || (bstride == M * n && M % fs::TW == 0))
+                              : (count == 1 || (bstride == M * n && n % fs::Q == 0 && n * count < ((int64_t)1 << 31))));
+        const uint64_t key[6] = {(uint64_t)(uintptr_t)x, (uint64_t)M, (uint64_t)n, (uint64_t)count,
+                                 (uint64_t)bstride, (uint64_t)P * 16 + sizeof(T) * 2 + LAY};
+        uint64_t *skey = S.key[LAY];
+        void *smap = S.tmap[LAY];
+        if (memcmp(key, skey, sizeof(key)) != 0) {
+            auto enc = tensor_map_encoder();
+            if (!enc) return set_error(PB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+            const auto dt = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+            const int rank = flat ? 2 : 3;
+            const int64_t bs = count > 1 ? bstride : P * (LAY == fs::LAY_CONTIG ? M : n);
+            CUresult r;
+            cuuint32_t estr[3] = {1, 1, 1};
+            if (LAY == fs::LAY_CONTIG) {
+                cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)(flat ? M * count : M), (cuuint64_t)(flat ? 1 : count)};
+                cuuint64_t strides[2] = {(cuuint64_t)(P * sizeof(T)), (cuuint64_t)(bs * sizeof(T))};
+                cuuint32_t box[3] = {(cuuint32_t)fs::Sw<T>::EB, (cuuint32_t)fs::TW, 1};
+                r = enc((CUtensorMap *)smap, dt, rank, (void *)x, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            } else {
+                cuuint64_t dims[3] = {(cuuint64_t)M, (cuuint64_t)(flat ? n * count : n), (cuuint64_t)(flat ? 1 : count)};
+                cuuint64_t strides[2] = {(cuuint64_t)(P * sizeof(T)), (cuuint64_t)(bs * sizeof(T))};
+                cuuint32_t box[3] = {(cuuint32_t)fs::TW, (cuuint32_t)fs::Q, 1};
+                r = enc((CUtensorMap *)smap, dt, rank, (void *)x, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            }
+            if (r != CUDA_SUCCESS) return set_error(PB_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+            memcpy(skey, key, sizeof(key));
+        }
+        A.flat = flat ? 1 : 0;
+        CUtensorMap tmap;
+        memcpy(&tmap, smap, sizeof(tmap));
+
+        A.rec = (const T *)h->fplan.rec;
+        A.coef = (const T *)h->coef;
+        A.ct = (const T *)h->fplan.ct;
+        A.rsp = (const T *)h->fplan.rsp;
+        A.scal = h->scal;
+        A.x = x;
+        A.xout = xout;
+        A.alpha = (T)alpha;
+        A.bstride = count > 1 ? bstride : P * (LAY == fs::LAY_CONTIG ? M : n);
+        A.pitch = P;
+        A.n = n;
+        A.M = M;
+        A.nsys = nsys;
+        A.items = items;
+        A.nclaims = nclaims;
+        for (int j = 0; j < 4; ++j) A.srow[j] = h->srow[j];
+        A.nq = nq;
+        A.count = (int)count;
+        A.Gb = (int)Gb;
+        A.G = (int)G;
+        const double gbytes = (double)fs::TW * (double)n * (double)es;
+        int64_t D = (int64_t)(FS_L2_BUDGET / gbytes);
+        A.D = (int)(D < 1 ? 1 : (D > G ? G : D));
+        A.qspec = PER ? (int)(h->srow[0] / fs::Q) : nq;
+        const int grid = (int)std::min<int64_t>(fs_sm_count(), nclaims);
+        // cooperative: all CTAs co-resident (the static work deal relies on it).
+        // Launched under the lock: the scratch (and its cached map) is not
+        // re-laid-out between this launch's setup and its enqueue
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(fs::NTHREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        PB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tmap, A));
+        PB_LAUNCH_CHECK();
+    }
+    return PB_OK;
+}
+
+
+template <typename T, int LAY>
+static int fs_launch_dl(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st, int64_t M,
+                        int64_t pitch)
+{
+    T *X = (T *)x;
+    using namespace fs;
+    int rc;
+    if (h->K == 2)
+        rc = h->periodic ? fc_launch_t<T, 2, true, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch)
+                         : fc_launch_t<T, 2, false, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch);
+    else
+        rc = h->periodic ? fc_launch_t<T, 1, true, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch)
+                         : fc_launch_t<T, 1, false, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch);
+    if (rc != PB_EUNSUPPORTED) return rc;
+    // beyond the cluster's shared-memory span: the global-scan kernel
+    if (h->K == 2)
+        return h->periodic ? fs_launch_t<T, 2, true, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch)
+                           : fs_launch_t<T, 2, false, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch);
+    return h->periodic ? fs_launch_t<T, 1, true, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch)
+                       : fs_launch_t<T, 1, false, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch);
+}
+
+int FS_NAME(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st, int64_t M, int64_t pitch)
+{
+    return fs_launch_dl<FS_T, FS_LAY>(h, x, count, bstride, st, M, pitch);
+}
+
+// diagnostics: the cluster configuration a solve of M systems x count would use
+int FS_INFO_NAME(const Band *h, int64_t M, int64_t count, int *info)
+{
+    if (h->K == 2)
+        return h->periodic ? fc_launch_t<FS_T, 2, true, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0,
+                                                                                 nullptr, M, 0, info)
+                           : fc_launch_t<FS_T, 2, false, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0,
+                                                                                  nullptr, M, 0, info);
+    return h->periodic ? fc_launch_t<FS_T, 1, true, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0, nullptr,
+                                                                             M, 0, info)
+                       : fc_launch_t<FS_T, 1, false, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0, nullptr,
+                                                                              M, 0, info);
+}
+
+#ifdef FS_CH1D_NAME
+int FS_CH1D_NAME(const Band *h, const void *c, void *cnew, double alpha, int64_t M, cudaStream_t st)
+{
+    int rc = fc_launch_t<FS_T, 2, true, fs::MODE_CH1D, fs::LAY_INTER>(h, (FS_T *)c, (FS_T *)cnew, alpha, 1, 0, st, M, 0);
+    if (rc != PB_EUNSUPPORTED) return rc;
+    return fs_launch_t<FS_T, 2, true, fs::MODE_CH1D, fs::LAY_INTER>(h, (FS_T *)c, (FS_T *)cnew, alpha, 1, 0, st, M, 0);
+}
+#endif
+
+}  // namespace pb

@@ -65,7 +65,6 @@ constexpr int REC = 6;   // P1 row record length
 constexpr int NC = 4;    // consumer warps (= items per claim)
 constexpr int NSW = 3;   // scan warps (1 + NC + NSW = 8 warps: the full 255-register budget)
 constexpr int NTHREADS = 32 * (NC + 1 + NSW);
-constexpr int LMAX = 3;  // windowed mode: the chunk maps of the LHS decay below 1e-18 within LMAX chunks
 
 // what the tile holds on arrival:
 //   MODE_SOLVE  the right-hand side f (pent_solve / tri_solve / the ADI y-sweep)
@@ -81,12 +80,12 @@ template <typename T>
 struct Cfg {
     static constexpr int TILE = Q * TW;             // elements
     static constexpr int COEF = Q * COEF_STRIDE;    // >= Q * REC
-    // inflow area: group-scan mode (yin, zin) blocks of 32 systems x 2, or
-    // windowed mode 2*LMAX yF blocks + LMAX zB blocks (chunk records, pairs)
-    static constexpr int INF = 3 * LMAX * TW * 2;
+    static constexpr int INF = TW * 4;              // (yin, zin) blocks of the tile's 32 systems
     static constexpr int XL = TW * 2;
     static constexpr int HALO = TW * 2;             // MODE_CH1D: rows r0 - 1 and r0 + kmax (periodic)
-    static constexpr int SLOT = TILE + COEF + INF + XL + HALO;
+    // (a multiple of 1 KB: every slot's tile must keep the 128B swizzle alignment)
+    static constexpr int SLOT = (TILE + COEF + INF + XL + HALO + 1024 / (int)sizeof(T) - 1) / (1024 / (int)sizeof(T)) *
+                                (1024 / (int)sizeof(T));
     static constexpr int NS = sizeof(T) == 8 ? 8 : 16;
     static_assert(NS % NC == 0, "ring slots must be a multiple of the consumer warps");
 };
@@ -113,8 +112,6 @@ struct Args {
     int64_t srow[4];
     int nq, count, Gb, G, D;
     int qspec;          // first chunk holding a cyclic row (cyclic only)
-    int win;            // windowed mode: inflows from the 2*win+1 neighbouring chunks (0: group scan)
-    const unsigned char *needxl;   // windowed + cyclic: chunk q's rows carry a cyclic correction
     int flat;           // one 2-D map over all batches: interleaved (M, n*count), row b*n + r (n % Q == 0);
                         // contiguous (n, M*count), system b*M + s (M % 32 == 0)
 };
@@ -578,109 +575,6 @@ __device__ void scan_group(const Args<T> &A, ScanSmem<T> &S, int g, int sw, int 
     }
 }
 
-// ---------------------------------------------------------------- windowed mode
-// The chunk maps of the LHS decay: ||Mf_{q+L-1}..Mf_q|| and ||Mb_q..Mb_{q+L-1}||
-// < 1e-18 for every q at L = A.win (checked when the handle is factored), so
-//   yin_q = sum_{p<q} Mf_{q-1}..Mf_{p+1} yF_p   and   zin_q = sum_{p>q} Mb_{q+1}..Mb_{p-1} c_p
-// (c_p = zB_p + H_p yin_p) are exact in fp64 when truncated to p in [q-L, q+L]:
-// the recurrences of the scan, run over that window from zero inflow.
-// yF(p) / zB(p) are (lane-private) loaders of the records.
-template <typename T, typename YF, typename ZB>
-__device__ __forceinline__ void window_inflow(const Args<T> &A, int q, YF yF, ZB zB, T &y0, T &y1, T &z0, T &z1)
-{
-    const int L = A.win, nq = A.nq;
-    T ya = T(0), yb = T(0), cz[LMAX][2];
-#pragma unroll
-    for (int d = 0; d < 2 * LMAX; ++d) {
-        if (d < 2 * L) {
-            const int p = q - L + d;
-            if (p >= 0 && p < nq) {
-                T m[4], f0, f1, t0, t1;
-                ldm4(A.ct + (int64_t)p * 12, m);
-                yF(d, p, f0, f1);
-                mv(m, ya, yb, t0, t1);
-                ya = t0 + f0;
-                yb = t1 + f1;
-            }
-            if (d == L - 1) y0 = ya, y1 = yb;        // after chunk q-1: yin_q
-            if (d >= L) {                            // after chunk q+e: yin_{q+1+e} -> c_{q+1+e}
-                const int e = d - L, pp = q + 1 + e;
-                if (pp < nq) {
-                    T h[4], b0, b1, t0, t1;
-                    ldm4(A.ct + (int64_t)pp * 12 + 8, h);
-                    zB(e, pp, b0, b1);
-                    mv(h, ya, yb, t0, t1);
-                    cz[e][0] = b0 + t0;
-                    cz[e][1] = b1 + t1;
-                }
-            }
-        }
-    }
-    T za = T(0), zb = T(0);
-#pragma unroll
-    for (int e = LMAX - 1; e >= 0; --e) {
-        const int pp = q + 1 + e;
-        if (e < L && pp < nq) {
-            T m[4], t0, t1;
-            ldm4(A.ct + (int64_t)pp * 12 + 4, m);
-            mv(m, za, zb, t0, t1);
-            za = t0 + cz[e][0];
-            zb = t1 + cz[e][1];
-        }
-    }
-    z0 = za, z1 = zb;
-}
-
-// Windowed mode, cyclic: Navon's pair x_l / Sherman–Morrison
-// of system `sys` of group g from the records near both ends.
-template <typename T, int K>
-__device__ void window_xl(const Args<T> &A, int64_t sys)
-{
-    const int L = A.win, nq = A.nq;
-    auto ldy = [&](int, int p, T &a, T &b) { ld_pair(A.car + rec_off(p, 0, sys, A.nsys), a, b); };
-    auto ldz = [&](int, int p, T &a, T &b) { ld_pair(A.car + rec_off(p, 1, sys, A.nsys), a, b); };
-    // (x_0, x_1) of the non-cyclic solution = c_0 + Mb_0 zin_0 (yin_0 = 0, c_0 = zB_0)
-    T y0, y1, z0, z1;
-    window_inflow<T>(A, 0, ldy, ldz, y0, y1, z0, z1);
-    T m[4], t0, t1, c0, c1;
-    ldm4(A.ct + 4, m);
-    ldz(0, 0, c0, c1);
-    mv(m, z0, z1, t0, t1);
-    const T y1c = c0 + t0, y2c = c1 + t1;
-    // true g on the cyclic rows: zero-inflow g + response to the chunk's inflow
-    T gv[4] = {T(0), T(0), T(0), T(0)};
-#pragma unroll
-    for (int jx = 0; jx < 4; ++jx) {
-        if (A.srow[jx] < 0) continue;
-        const int qj = (int)(A.srow[jx] / Q);
-        T a0 = T(0), a1 = T(0);
-        for (int p = max(0, qj - L); p < qj; ++p) {
-            T mm[4], f0, f1, u0, u1;
-            ldm4(A.ct + (int64_t)p * 12, mm);
-            ldy(0, p, f0, f1);
-            mv(mm, a0, a1, u0, u1);
-            a0 = u0 + f0;
-            a1 = u1 + f1;
-        }
-        gv[jx] = __ldcg(A.spec + sys * 4 + jx) + A.rsp[jx * 2] * a0 + A.rsp[jx * 2 + 1] * a1;
-    }
-    const double *sc = A.scal;
-    T xl0, xl1;
-    if (K == 2) {
-        const T ym1 = gv[1], ym2 = gv[0] - T(sc[10]) * gv[1];
-        const T q0 = gv[2] - (T(sc[4]) * y1c + T(sc[5]) * ym2 + T(sc[6]) * ym1);
-        const T q1 = gv[3] - (T(sc[7]) * y1c + T(sc[8]) * y2c + T(sc[9]) * ym1);
-        xl0 = T(sc[0]) * q0 + T(sc[1]) * q1;
-        xl1 = T(sc[2]) * q0 + T(sc[3]) * q1;
-    } else {
-        xl0 = (y1c + T(sc[0]) * gv[0]) / T(sc[1]);
-        xl1 = T(0);
-    }
-    __stcg(A.xl + sys * 2 + 0, xl0);
-    __stcg(A.xl + sys * 2 + 1, xl1);
-    (void)nq;
-}
-
 // ---------------------------------------------------------------- the kernel
 template <typename T>
 struct Smem {
@@ -730,25 +624,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) fs_kernel(const __grid_constant__
         // ---------------- producer: claim NC items at a time, one per consumer warp
         if (lane == 0) {
             const unsigned epoch = ld_relaxed(A.tick + 3) + 1u;
-            const unsigned need = epoch * (unsigned)A.nq;   // P1 tiles of a group done by this launch (mod 2^32)
             const uint64_t pol1 = policy_evict_last(), pol2 = policy_evict_first();
             for (int64_t k = 0;; ++k) {
                 const int64_t c = blockIdx.x + k * gridDim.x;   // this CTA's k-th claim (static)
                 const bool done = c >= A.nclaims;
                 Item it[NC];
-                unsigned f1[NC], f2[NC];
-                bool nx[NC];
+                unsigned fl[NC];
 #pragma unroll
                 for (int w = 0; w < NC; ++w) {
                     const int64_t i = c * NC + w;
                     const bool live = !done && i < A.items;
                     it[w] = live ? decode(i, A.nq, A.G, A.D) : Item{0, 0, 0};
-                    const bool p2 = live && it[w].p2;
-                    // windowed: all P1 tiles of the group (monotone counter), + the group's
-                    // x_l where the chunk carries a cyclic correction; else the group scan
-                    nx[w] = PER && (!A.win || (p2 && A.needxl[it[w].q]));
-                    f1[w] = (p2 && A.win) ? ld_relaxed(A.cnt + it[w].g) : need;
-                    f2[w] = (p2 && (!A.win || nx[w])) ? ld_relaxed(A.flag + it[w].g) : epoch;
+                    fl[w] = (live && it[w].p2) ? ld_relaxed(A.flag + it[w].g) : epoch;
                 }
 #pragma unroll
                 for (int w = 0; w < NC; ++w) {
@@ -762,10 +649,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fs_kernel(const __grid_constant__
                     }
                     const Item id = it[w];
                     if (id.p2) {
-                        // the records (and x_l) must be complete before they are copied
-                        if (f1[w] != need)
-                            while (ld_acquire(A.cnt + id.g) != need) __nanosleep(64);
-                        if (f2[w] != epoch)
+                        // the group's scan must be complete before its inflows are copied
+                        if (fl[w] != epoch)
                             while (ld_acquire(A.flag + id.g) != epoch) __nanosleep(64);
                         fence_acquire();
                         fence_proxy_global();
@@ -777,18 +662,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fs_kernel(const __grid_constant__
                     T *slot = sm.slot[sl];
                     const uint32_t cb = up16((uint32_t)(kmax * (id.p2 ? COEF_STRIDE : REC) * sizeof(T)));
                     uint32_t bytes = TILE * sizeof(T) + cb;
-                    // P2 inflow data: group scan -> (yin, zin) blocks; windowed -> the yF
-                    // blocks of chunks [q-L, q+L-1] and zB blocks of [q+1, q+L] in range
-                    int nblk = 0;
-                    if (id.p2) {
-                        if (A.win) {
-                            for (int d = 0; d < 2 * A.win; ++d) nblk += (id.q - A.win + d >= 0 && id.q - A.win + d < A.nq);
-                            for (int e = 0; e < A.win; ++e) nblk += (id.q + 1 + e < A.nq);
-                        } else {
-                            nblk = 2;
-                        }
-                        bytes += (uint32_t)(nblk * 2 * TW * sizeof(T)) + (nx[w] ? Cfg<T>::XL * sizeof(T) : 0);
-                    }
+                    if (id.p2) bytes += (Cfg<T>::INF + (PER ? Cfg<T>::XL : 0)) * sizeof(T);
                     if (MODE == MODE_CH1D) bytes += Cfg<T>::HALO * sizeof(T);
                     bar_expect_tx(&sm.full[sl], bytes);
                     const uint64_t pol = id.p2 ? pol2 : pol1;
@@ -819,21 +693,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fs_kernel(const __grid_constant__
                         T *ia = slot + TILE + Cfg<T>::COEF;
                         const int64_t s0 = (int64_t)id.g * TW;
                         constexpr uint32_t BB = 2 * TW * sizeof(T);   // one (q, half) block of the group
-                        if (A.win) {
-                            for (int d = 0; d < 2 * A.win; ++d) {
-                                const int p = id.q - A.win + d;
-                                if (p >= 0 && p < A.nq) bulk_load(ia + d * 2 * TW, A.car + rec_off(p, 0, s0, A.nsys), BB, &sm.full[sl]);
-                            }
-                            for (int e = 0; e < A.win; ++e) {
-                                const int p = id.q + 1 + e;
-                                if (p < A.nq)
-                                    bulk_load(ia + (2 * LMAX + e) * 2 * TW, A.car + rec_off(p, 1, s0, A.nsys), BB, &sm.full[sl]);
-                            }
-                        } else {
-                            bulk_load(ia, A.car + rec_off(id.q, 0, s0, A.nsys), BB, &sm.full[sl]);
-                            bulk_load(ia + 2 * TW, A.car + rec_off(id.q, 1, s0, A.nsys), BB, &sm.full[sl]);
-                        }
-                        if (nx[w])
+                        bulk_load(ia, A.car + rec_off(id.q, 0, s0, A.nsys), BB, &sm.full[sl]);
+                        bulk_load(ia + 2 * TW, A.car + rec_off(id.q, 1, s0, A.nsys), BB, &sm.full[sl]);
+                        if (PER)
                             bulk_load(slot + TILE + Cfg<T>::COEF + Cfg<T>::INF, A.xl + s0 * 2, Cfg<T>::XL * sizeof(T),
                                       &sm.full[sl]);
                     }
@@ -895,16 +757,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fs_kernel(const __grid_constant__
             for (int k = 0; k < Q; ++k) v[k] = tld<T, LAY>(d, k, lane);
             const T *inf = c + Cfg<T>::COEF;
             T y0, y1, z0, z1, xl0 = T(0), xl1 = T(0);
-            if (A.win) {
-                auto ldy = [&](int d, int, T &a, T &bb) { lds2(inf + d * 2 * TW + lane * 2, a, bb); };
-                auto ldz = [&](int e, int, T &a, T &bb) { lds2(inf + (2 * LMAX + e) * 2 * TW + lane * 2, a, bb); };
-                window_inflow<T>(A, id.q, ldy, ldz, y0, y1, z0, z1);
-                if (PER && A.needxl[id.q]) lds2(inf + Cfg<T>::INF + lane * 2, xl0, xl1);
-            } else {
-                lds2(inf + lane * 2, y0, y1);
-                lds2(inf + 2 * TW + lane * 2, z0, z1);
-                if (PER) lds2(inf + Cfg<T>::INF + lane * 2, xl0, xl1);
-            }
+            lds2(inf + lane * 2, y0, y1);
+            lds2(inf + 2 * TW + lane * 2, z0, z1);
+            if (PER) lds2(inf + Cfg<T>::INF + lane * 2, xl0, xl1);
             if (kmax == Q) tile_solve<T, K, PER, true>(v, c, Q, y0, y1, z0, z1, xl0, xl1);
             else tile_solve<T, K, PER, false>(v, c, kmax, y0, y1, z0, z1, xl0, xl1);
             if (PER && K == 2 && r0 + Q > A.n - 2) {
@@ -960,27 +815,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) fs_kernel(const __grid_constant__
         const int sw = warp - NC - 1;
         const unsigned epoch = ld_relaxed(A.tick + 3) + 1u;
         const unsigned need = epoch * (unsigned)A.nq;
-        if (A.win) {
-            // windowed: no scan; cyclic systems get x_l per group from the end records
-            if (PER && sw == 0) {
-                for (int g = blockIdx.x; g < A.G; g += gridDim.x) {   // groups in order (static)
-                    while (ld_acquire(A.cnt + g) != need) __nanosleep(128);
-                    window_xl<T, K>(A, (int64_t)g * TW + lane);
-                    __threadfence();
-                    fence_proxy_global();
-                    __syncwarp();
-                    if (lane == 0) st_release(A.flag + g, epoch);
-                }
-            }
-        } else {
-            for (int g = blockIdx.x; g < A.G; g += gridDim.x) {   // groups in order (static)
-                while (ld_acquire(A.cnt + g) != need) __nanosleep(128);
-                scan_group<T, K, PER>(A, sm.scan, g, sw, lane);
-                __threadfence();
-                fence_proxy_global();
-                scan_bar();   // all records / x_l of the group written
-                if (sw == 0 && lane == 0) st_release(A.flag + g, epoch);
-            }
+        for (int g = blockIdx.x; g < A.G; g += gridDim.x) {   // groups in order (static)
+            while (ld_acquire(A.cnt + g) != need) __nanosleep(128);
+            scan_group<T, K, PER>(A, sm.scan, g, sw, lane);
+            __threadfence();
+            fence_proxy_global();
+            scan_bar();   // all records / x_l of the group written
+            if (sw == 0 && lane == 0) st_release(A.flag + g, epoch);
         }
     }
     // the last CTA out resets the tickets for the next launch (stream-ordered)
