@@ -114,6 +114,22 @@ PB_API int pent_solve(pb_penta_t h, void *rhs, int layout, void *stream);
 PB_API int pent_solve_many(pb_penta_t h, void *rhs, int layout, int64_t count, int64_t batch_stride,
                     void *stream);
 
+/* pent_refactor — re-factor a PER-SYSTEM handle (lhs_count == batch) in place
+ * with new diagonals (cuPentBatchRewrite: matrices that change
+ * every step).  a..e: DEVICE fp64 arrays laid out as for pent_factor.  Hot
+ * path: no allocation after the first call, no host sync, and no pivot
+ * report (a zero pivot yields non-finite solutions).  Shared-LHS handles:
+ * PB_EUNSUPPORTED (factor a new one).                                      */
+PB_API int pent_refactor(pb_penta_t h, const double *a, const double *b, const double *c, const double *d,
+                         const double *e, void *stream);
+
+/* pent_factor_uniform — a shared LHS whose diagonals are constants (a, b, c,
+ * d, e) (cuPentUniformBatch; periodic: the wrap entries take the
+ * same constants, the matrix of P:1446-1453).  Same semantics and errors as
+ * pent_factor with lhs_count = 1.                                          */
+PB_API int pent_factor_uniform(int64_t batch, int64_t n, double a, double b, double c, double d, double e,
+                               int periodic, int dtype, void *stream, pb_penta_t *out);
+
 /* pent_solve_strided — the general batched form (systems stored
  * interleaved, one per thread, or one after another).  System s of batch b
  * occupies rhs[b*outer_stride + s*inner_stride + i*row_stride], i = 0..n-1,
@@ -139,7 +155,11 @@ PB_API int pent_solve_strided(pb_penta_t h, void *rhs, const pb_layout *L, void 
  * solve for one batch of the handle in `layout`: info[0] = thread-block
  * cluster size CS (0 = N beyond the cluster span, the global-scan kernel
  * serves), info[1] = 64-row chunks per CTA, info[2] = clusters launched;
- * all -1 when the handle has no fused plan (per-system LHS).               */
+ * all -1 when the handle has no fused plan: per-system LHS, or chunk maps
+ * of the factored LHS that grow (max-abs entry >= 1 over a 64-row chunk,
+ * e.g. kappa ~ 1e6+) -- such handles are solved one thread per system, the
+ * sequential order of P:1712-1724, because the chunked carry scan would
+ * amplify rounding.                                                        */
 PB_API int pent_solve_info(pb_penta_t h, int layout, int *info);
 
 PB_API int pent_destroy(pb_penta_t h);
@@ -156,6 +176,11 @@ PB_API int tri_factor(int64_t batch, int64_t n, const double *a, const double *b
                int64_t lhs_count, int periodic, int dtype, void *stream, pb_tri_t *out);
 PB_API int tri_solve(pb_tri_t h, void *rhs, int layout, void *stream);
 PB_API int tri_solve_strided(pb_tri_t h, void *rhs, const pb_layout *L, void *stream);
+/* tri_refactor / tri_factor_uniform: as pent_refactor / pent_factor_uniform
+ * (the CN diffusion matrix (-s, 1+2s, -s)).                  */
+PB_API int tri_refactor(pb_tri_t h, const double *a, const double *b, const double *c, void *stream);
+PB_API int tri_factor_uniform(int64_t batch, int64_t n, double a, double b, double c, int periodic, int dtype,
+                              void *stream, pb_tri_t *out);
 PB_API int tri_destroy(pb_tri_t h);
 
 /* ------------------------------------------------------------------------

@@ -21,8 +21,9 @@ PB_INTERLEAVED, PB_CONTIGUOUS = 0, 1
 PB_NONPERIODIC, PB_PERIODIC = 0, 1
 
 # every symbol include/pentab.h declares
-EXPORTS = ("pent_factor", "pent_solve", "pent_solve_many", "pent_solve_strided", "pent_solve_info", "pent_destroy", "tri_factor",
-           "tri_solve", "tri_solve_strided", "tri_destroy", "stencil_apply", "ch_workspace_bytes", "ch_adi_step", "ch1d_step", "ch_dist_pass_a",
+EXPORTS = ("pent_factor", "pent_solve", "pent_solve_many", "pent_solve_strided", "pent_solve_info", "pent_refactor", "pent_factor_uniform",
+           "pent_destroy", "tri_factor", "tri_solve", "tri_solve_strided", "tri_refactor", "tri_factor_uniform",
+           "tri_destroy", "stencil_apply", "ch_workspace_bytes", "ch_adi_step", "ch1d_step", "ch_dist_pass_a",
            "ch_dist_pack", "ch_dist_ysweep", "ch_dist_combine", "pb_last_error", "pb_launch_count", "pb_reset_launch_count",
            "pb_device_ok")
 
@@ -81,6 +82,10 @@ def lib() -> ctypes.CDLL:
         L.pent_solve_strided.argtypes = [P, P, ctypes.POINTER(pb_layout), P]
         L.tri_solve_strided.argtypes = [P, P, ctypes.POINTER(pb_layout), P]
         L.pent_solve_info.argtypes = [P, I, ctypes.POINTER(ctypes.c_int)]
+        L.pent_refactor.argtypes = [P, P, P, P, P, P, P]
+        L.pent_factor_uniform.argtypes = [I64, I64, D, D, D, D, D, I, I, P, ctypes.POINTER(P)]
+        L.tri_refactor.argtypes = [P, P, P, P, P]
+        L.tri_factor_uniform.argtypes = [I64, I64, D, D, D, I, I, P, ctypes.POINTER(P)]
         L.pent_destroy.argtypes = [P]
         L.tri_factor.argtypes = [I64, I64, P, P, P, I64, I, I, P, ctypes.POINTER(P)]
         L.tri_solve.argtypes = [P, P, I, P]
@@ -188,6 +193,10 @@ class PentaHandle(_Banded):
         _check(lib().pent_solve_info(self._h, _layout(layout), w))
         return tuple(w)
 
+    def refactor(self, a, b, c, d, e, stream=None):
+        """pent_refactor: new per-system diagonals (device fp64), in place, no sync."""
+        _check(lib().pent_refactor(self._h, _ptr(a), _ptr(b), _ptr(c), _ptr(d), _ptr(e), _stream(a, stream)))
+
     def solve_many(self, rhs, count, batch_stride, layout="interleaved", stream=None):
         _check(lib().pent_solve_many(self._h, _ptr(rhs), _layout(layout), count, batch_stride, _stream(rhs, stream)))
         return rhs
@@ -196,6 +205,10 @@ class PentaHandle(_Banded):
 class TriHandle(_Banded):
     _destroy = "tri_destroy"
     _strided = "tri_solve_strided"
+
+    def refactor(self, a, b, c, stream=None):
+        """tri_refactor: new per-system diagonals (device fp64), in place, no sync."""
+        _check(lib().tri_refactor(self._h, _ptr(a), _ptr(b), _ptr(c), _stream(a, stream)))
 
     def solve(self, rhs, layout="interleaved", stream=None):
         _check(lib().tri_solve(self._h, _ptr(rhs), _layout(layout), _stream(rhs, stream)))
@@ -213,6 +226,24 @@ def pent_factor(a, b, c, d, e, *, batch, n, lhs_count=1, periodic=False, dtype="
     _check(lib().pent_factor(batch, n, _ptr(a), _ptr(b), _ptr(c), _ptr(d), _ptr(e), lhs_count, int(bool(periodic)),
                              _dt(dtype), _stream(a, stream), ctypes.byref(h)))
     return PentaHandle(h, batch, n, _dt(dtype))
+
+
+def pent_factor_uniform(a, b, c, d, e, *, batch, n, periodic=False, dtype="f64", stream=None) -> PentaHandle:
+    """Shared LHS with constant diagonals (cuPentUniformBatch)."""
+    h = ctypes.c_void_p()
+    s = ctypes.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream) if stream is not None else \
+        ctypes.c_void_p(0)
+    _check(lib().pent_factor_uniform(batch, n, a, b, c, d, e, int(bool(periodic)), _dt(dtype), s, ctypes.byref(h)))
+    return PentaHandle(h, batch, n, _dt(dtype))
+
+
+def tri_factor_uniform(a, b, c, *, batch, n, periodic=False, dtype="f64", stream=None) -> TriHandle:
+    """Shared tridiagonal LHS with constant diagonals (e.g. CN diffusion)."""
+    h = ctypes.c_void_p()
+    s = ctypes.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream) if stream is not None else \
+        ctypes.c_void_p(0)
+    _check(lib().tri_factor_uniform(batch, n, a, b, c, int(bool(periodic)), _dt(dtype), s, ctypes.byref(h)))
+    return TriHandle(h, batch, n, _dt(dtype))
 
 
 def tri_factor(a, b, c, *, batch, n, lhs_count=1, periodic=False, dtype="f64", stream=None) -> TriHandle:

@@ -212,8 +212,9 @@ __device__ __forceinline__ void band_core(T (&v)[MR], const CoreArgs<T> &A, Core
         for (int k = 0; k < MR; ++k) {
             T f0, f1, f2;
             ldcoef_f(coef + k * COEF_STRIDE, f0, f1, f2);
-            T g = f0 * v[k] - f1 * y1;
+            T g = f0 * v[k];
             if (K == 2) g -= f2 * y0;
+            g -= f1 * y1;   // newest carry last: one FMA on the chain
             y0 = y1;
             y1 = g;
         }
@@ -254,8 +255,9 @@ __device__ __forceinline__ void band_core(T (&v)[MR], const CoreArgs<T> &A, Core
         for (int k = 0; k < MR; ++k) {
             T f0, f1, f2;
             ldcoef_f(coef + k * COEF_STRIDE, f0, f1, f2);
-            T g = f0 * v[k] - f1 * y1;
+            T g = f0 * v[k];
             if (K == 2) g -= f2 * y0;
+            g -= f1 * y1;   // newest carry last: one FMA on the chain
             y0 = y1;
             y1 = g;
             v[k] = g;
@@ -285,8 +287,9 @@ __device__ __forceinline__ void band_core(T (&v)[MR], const CoreArgs<T> &A, Core
         for (int k = MR - 1; k >= 0; --k) {
             T b1, b2;
             ldcoef_b(coef + k * COEF_STRIDE, b1, b2);
-            T xx = v[k] - b1 * z0;
+            T xx = v[k];
             if (K == 2) xx -= b2 * z1;
+            xx -= b1 * z0;
             z1 = z0;
             z0 = xx;
         }
@@ -370,8 +373,9 @@ __device__ __forceinline__ void band_core(T (&v)[MR], const CoreArgs<T> &A, Core
         for (int k = MR - 1; k >= 0; --k) {
             T b1, b2;
             ldcoef_b(coef + k * COEF_STRIDE, b1, b2);
-            T xx = v[k] - b1 * z0;
+            T xx = v[k];
             if (K == 2) xx -= b2 * z1;
+            xx -= b1 * z0;
             z1 = z0;
             z0 = xx;
             if (PER) {

@@ -49,9 +49,16 @@ struct Band {
     Plan plan;
     FusedPlan fplan;
     int64_t srow[4] = {-1, -1, -1, -1};
+    // the 64-row chunk maps of the factored LHS grow (max |Mf_q|, |Mb_q| >= 1):
+    // chunked solves would amplify rounding through the carry scan, so this
+    // handle is solved sequentially, one thread per system (the thesis's kernel)
+    bool seq_only = false;
+    double chunk_growth = 0.0;
     // per-system LHS
     void *pcoef = nullptr;    // dtype, [(i*8 + j) * batch + s]
     double *pscal = nullptr;  // [j * batch + s]
+    double *pcoefD = nullptr; // fp64 factor scratch of fp32 per-system handles (pent_refactor)
+    int64_t *rstatus = nullptr;   // device status of pent_refactor (never read back on the hot path)
     bool shared() const { return lhs_count == 1; }
     ~Band()
     {
@@ -63,6 +70,8 @@ struct Band {
         cudaFree(plan.mbc);
         cudaFree(pcoef);
         cudaFree(pscal);
+        cudaFree(pcoefD);
+        cudaFree(rstatus);
         cudaFree(fplan.rec);
         cudaFree(fplan.ct);
         cudaFree(fplan.rsp);

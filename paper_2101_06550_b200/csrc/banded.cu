@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include <cudaTypedefs.h>
 
@@ -461,6 +462,37 @@ static int launch_persys_t(const Band *h, T *x, const pb_layout &L, cudaStream_t
 }
 
 // ---------------------------------------------------------------- factor / solve drivers
+// max over the 64-row chunks of the max-abs entry of the forward and backward
+// homogeneous chunk maps (fp64, from the master coefficients on the host)
+static double chunk_map_growth(const Band *h)
+{
+    const int64_t n = h->n, rows = h->rows_alloc, nq = (n + 63) / 64;
+    std::vector<double> cf((size_t)rows * COEF_STRIDE);
+    if (cudaMemcpy(cf.data(), h->coefD, sizeof(double) * cf.size(), cudaMemcpyDeviceToHost) != cudaSuccess) {
+        cudaGetLastError();
+        return 0.0;
+    }
+    auto C = [&](int64_t r, int j) { return (h->K == 1 && (j == 2 || j == 5)) ? 0.0 : cf[(size_t)r * COEF_STRIDE + j]; };
+    double g = 0.0;
+    for (int64_t q = 0; q < nq; ++q) {
+        const int64_t r0 = q * 64, kmax = std::min<int64_t>(64, n - r0);
+        for (int col = 0; col < 2; ++col) {
+            double y0 = col == 0, y1 = col == 1;
+            for (int64_t i = 0; i < kmax; ++i) {
+                const double gg = -C(r0 + i, 1) * y1 - C(r0 + i, 2) * y0;
+                y0 = y1, y1 = gg;
+            }
+            double z0 = col == 0, z1 = col == 1;
+            for (int64_t i = kmax - 1; i >= 0; --i) {
+                const double x = -C(r0 + i, 4) * z0 - C(r0 + i, 5) * z1;
+                z1 = z0, z0 = x;
+            }
+            g = std::max(g, std::max(std::max(fabs(y0), fabs(y1)), std::max(fabs(z0), fabs(z1))));
+        }
+    }
+    return g;
+}
+
 static int factor_impl(Band *h, const double *a, const double *b, const double *c, const double *d, const double *e,
                        cudaStream_t st, int forced_k = -1, int forced_C = 0)
 {
@@ -494,6 +526,8 @@ static int factor_impl(Band *h, const double *a, const double *b, const double *
         }
         h->rows_alloc = k >= 0 ? (int64_t)C * rc_rows : n;
         if (h->rows_alloc < n) h->rows_alloc = n;
+        const int64_t chunk_rows = (n + 63) / 64 * 64;   // whole 64-row chunks for the fused solve tables
+        if (h->rows_alloc < chunk_rows) h->rows_alloc = chunk_rows;
         if (h->periodic) {
             if (h->K == 2) {
                 h->srow[0] = n - 4;
@@ -586,6 +620,10 @@ static int factor_impl(Band *h, const double *a, const double *b, const double *
         set_pivot(sys, -1);
         return code;
     }
+    if (h->shared() && h->n > 64) {
+        h->chunk_growth = chunk_map_growth(h);
+        h->seq_only = h->chunk_growth >= 1.0;
+    }
     return PB_OK;
 }
 
@@ -666,7 +704,7 @@ int band_solve_layout(const Band *h, void *rhs, const pb_layout &L, cudaStream_t
     const bool inter = L.inner_stride == 1 && L.row_stride >= L.n_inner;
     const bool contig = L.row_stride == 1 && L.inner_stride >= n;
     const size_t es = dtype_size(h->dtype);
-    if (inter && L.n_outer == 1 && h->shared() && h->fplan.ok && L.n_inner >= 4096 && !is_device_ptr(rhs))
+    if (inter && L.n_outer == 1 && h->shared() && h->fplan.ok && !h->seq_only && L.n_inner >= 4096 && !is_device_ptr(rhs))
         return pipelined_host_solve(h, rhs, L, st);
     const int64_t span = (L.n_outer - 1) * L.outer_stride + (L.n_inner - 1) * L.inner_stride + (n - 1) * L.row_stride + 1;
     Staged sx;
@@ -674,14 +712,14 @@ int band_solve_layout(const Band *h, void *rhs, const pb_layout &L, cudaStream_t
     if (rc) return rc;
     sx.out_to(rhs);
     const bool a16 = (uintptr_t)sx.dev % 16 == 0 && (L.n_outer == 1 || (L.outer_stride * es) % 16 == 0);
-    const bool fused = h->shared() && h->fplan.ok && a16 &&
+    const bool fused = h->shared() && h->fplan.ok && !h->seq_only && a16 &&
                        ((inter && (L.row_stride * es) % 16 == 0) || (contig && (L.inner_stride * es) % 16 == 0));
     const bool packed = L.n_inner == h->batch && ((inter && L.row_stride == L.n_inner) || (contig && L.inner_stride == n)) &&
                         (L.n_outer == 1 || L.outer_stride >= L.n_inner * n);
     if (fused) {
         rc = launch_fused(h, sx.dev, inter ? PB_INTERLEAVED : PB_CONTIGUOUS, L.n_outer, L.outer_stride, st, L.n_inner,
                           inter ? L.row_stride : L.inner_stride);
-    } else if (h->shared() && h->plan.C > 0 && packed) {
+    } else if (h->shared() && h->plan.C > 0 && packed && !h->seq_only) {
         const int layout = inter ? PB_INTERLEAVED : PB_CONTIGUOUS;
         rc = h->dtype == PB_F64
                  ? (h->K == 2 ? launch_tile_f64_k2(h, sx.dev, layout, L.n_outer, L.outer_stride, st)
@@ -746,6 +784,67 @@ static int make_band(int K, int64_t batch, int64_t n, const double *a, const dou
     return PB_OK;
 }
 
+// Uniform-scalar LHS (cuPentUniformBatch / cuThomasConstantBatch with equal
+// entries on each diagonal): the scalars become the diagonals of
+// one shared LHS; the factorisation is the same 14-step LR (it is not uniform
+// near the ends).
+__global__ void fill_diags_kernel(double *dg, int64_t n, double a, double b, double c, double d, double e)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        dg[i] = a;
+        dg[n + i] = b;
+        dg[2 * n + i] = c;
+        dg[3 * n + i] = d;
+        dg[4 * n + i] = e;
+    }
+}
+
+template <typename H>
+static int make_uniform(int K, int64_t batch, int64_t n, double a, double b, double c, double d, double e, int periodic,
+                        int dtype, cudaStream_t st, H **out)
+{
+    if (!out) return set_error(PB_EINVAL, "null out");
+    *out = nullptr;
+    if (n < 1) return set_error(PB_EINVAL, "n = %lld too small", (long long)n);
+    if (pb_device_ok() != PB_OK) return PB_ECUDA;
+    double *dg = nullptr;
+    PB_CUDA_TRY(cudaMallocAsync(&dg, sizeof(double) * 5 * n, st));
+    fill_diags_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, st>>>(dg, n, a, b, c, d, e);
+    PB_LAUNCH_CHECK();
+    int rc = make_band<H>(K, batch, n, dg, dg + n, dg + 2 * n, dg + 3 * n, dg + 4 * n, 1, periodic, dtype, st, out);
+    cudaFreeAsync(dg, st);
+    return rc;
+}
+
+// Re-factor a per-system handle in place (cuPentBatchRewrite: the
+// LHS changes every step): the same device kernels as pent_factor into the
+// handle's own buffers -- no allocation after the first call, no host sync, no
+// pivot report (a zero pivot yields non-finite solutions, r16).
+static int refactor_band(Band *h, const double *a, const double *b, const double *c, const double *d, const double *e,
+                         cudaStream_t st)
+{
+    if (!h) return set_error(PB_EINVAL, "null handle");
+    if (h->shared()) return set_error(PB_EUNSUPPORTED, "refactor is for per-system LHS handles (factor a new shared one)");
+    if (!a || !b || !c || (h->K == 2 && (!d || !e))) return set_error(PB_EINVAL, "null diagonal");
+    const int64_t n = h->n, M = h->batch;
+    if (M == 0) return PB_OK;
+    if (!h->rstatus) PB_CUDA_TRY(cudaMalloc(&h->rstatus, sizeof(int64_t) * 8));
+    double *dst = h->dtype == PB_F64 ? (double *)h->pcoef : h->pcoefD;
+    if (!dst) {
+        PB_CUDA_TRY(cudaMalloc(&h->pcoefD, sizeof(double) * COEF_STRIDE * n * M));
+        dst = h->pcoefD;
+    }
+    factor_persys_kernel<<<(unsigned)((M + 127) / 128), 128, 0, st>>>(h->K, n, M, h->periodic, a, b, c,
+                                                                      h->K == 2 ? d : nullptr, h->K == 2 ? e : nullptr,
+                                                                      dst, h->pscal, h->rstatus);
+    PB_LAUNCH_CHECK();
+    if (h->dtype != PB_F64) {
+        cast_kernel<<<256, 256, 0, st>>>(dst, (float *)h->pcoef, COEF_STRIDE * n * M);
+        PB_LAUNCH_CHECK();
+    }
+    return PB_OK;
+}
+
 // Constant cyclic pentadiagonal (s, -4s, 1+6s, -4s, s): the ADI operators
 // L_x = L_y = I + 2/3 D gamma dt d_xxxx, factored with a forced tile
 // configuration for the fused sweeps of ch_adi.cu.
@@ -802,6 +901,18 @@ int pent_solve_many(pb_penta_t h, void *rhs, int layout, int64_t count, int64_t 
     return pb::band_solve(h, rhs, layout, count, batch_stride, (cudaStream_t)stream);
 }
 
+int pent_refactor(pb_penta_t h, const double *a, const double *b, const double *c, const double *d, const double *e,
+                  void *stream)
+{
+    return pb::refactor_band(h, a, b, c, d, e, (cudaStream_t)stream);
+}
+
+int pent_factor_uniform(int64_t batch, int64_t n, double a, double b, double c, double d, double e, int periodic,
+                        int dtype, void *stream, pb_penta_t *out)
+{
+    return pb::make_uniform<pb_penta_s>(2, batch, n, a, b, c, d, e, periodic, dtype, (cudaStream_t)stream, out);
+}
+
 int pent_solve_strided(pb_penta_t h, void *rhs, const pb_layout *L, void *stream)
 {
     if (!L) return pb::set_error(PB_EINVAL, "null layout");
@@ -813,7 +924,7 @@ int pent_solve_info(pb_penta_t h, int layout, int *info)
     if (!h || !info || (layout != PB_INTERLEAVED && layout != PB_CONTIGUOUS))
         return pb::set_error(PB_EINVAL, "bad argument");
     info[0] = info[1] = info[2] = -1;
-    if (!h->shared() || !h->fplan.ok) return PB_OK;
+    if (!h->shared() || !h->fplan.ok || h->seq_only) return PB_OK;
     return pb::fused_info(h, layout, h->batch, 1, info);
 }
 
@@ -832,6 +943,17 @@ int tri_factor(int64_t batch, int64_t n, const double *a, const double *b, const
 int tri_solve(pb_tri_t h, void *rhs, int layout, void *stream)
 {
     return pb::band_solve(h, rhs, layout, 1, 0, (cudaStream_t)stream);
+}
+
+int tri_refactor(pb_tri_t h, const double *a, const double *b, const double *c, void *stream)
+{
+    return pb::refactor_band(h, a, b, c, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+int tri_factor_uniform(int64_t batch, int64_t n, double a, double b, double c, int periodic, int dtype, void *stream,
+                       pb_tri_t *out)
+{
+    return pb::make_uniform<pb_tri_s>(1, batch, n, a, b, c, 0.0, 0.0, periodic, dtype, (cudaStream_t)stream, out);
 }
 
 int tri_solve_strided(pb_tri_t h, void *rhs, const pb_layout *L, void *stream)

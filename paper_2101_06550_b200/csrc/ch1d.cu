@@ -8,6 +8,7 @@
 // step moves read C^n + write C^{n+1} through HBM (16 B per point fp64).
 #include <string.h>
 
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -40,6 +41,19 @@ static int ch1d_band(int64_t n, double sigma, int dtype, cudaStream_t st, Band *
     return PB_OK;
 }
 
+// f_i = C_i + alpha (N_{i-1} - 2 N_i + N_{i+1}), N = C^3 - C, periodic in i
+// (interleaved [i][s]); used when the handle is solved sequentially (seq_only)
+template <typename T>
+__global__ void ch1d_rhs_kernel(const T *__restrict__ c, T *__restrict__ f, int64_t n, int64_t M, T alpha)
+{
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * M; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / M, s = e - i * M;
+        const T um = c[(i == 0 ? n - 1 : i - 1) * M + s], u = c[e], up = c[(i == n - 1 ? 0 : i + 1) * M + s];
+        const T nm = um * um * um - um, n0 = u * u * u - u, np = up * up * up - up;
+        f[e] = u + alpha * (nm - T(2) * n0 + np);
+    }
+}
+
 }  // namespace pb
 
 extern "C" int ch1d_step(pb_ch1d_state *s, double dt, const pb_ch1d_params *p, int64_t nsteps, void *stream)
@@ -61,9 +75,29 @@ extern "C" int ch1d_step(pb_ch1d_state *s, double dt, const pb_ch1d_params *p, i
     Band *h = nullptr;
     int rc = ch1d_band(s->n, sigma, s->dtype, st, &h);
     if (rc) return rc;
-    if (!h->fplan.ok) return set_error(PB_EUNSUPPORTED, "no streaming plan for n = %lld", (long long)s->n);
+    const bool fused = h->fplan.ok && !h->seq_only;
     for (int64_t k = 0; k < nsteps; ++k) {
-        if ((rc = launch_fused_ch1d(h, s->c, s->work, alpha, s->batch, st))) return rc;
+        if (fused) {
+            if ((rc = launch_fused_ch1d(h, s->c, s->work, alpha, s->batch, st))) return rc;
+        } else {
+            // growing chunk maps (kappa ~ 1e6+, e.g. Table 6.1's N = 4096): RHS kernel +
+            // the sequential thread-per-system solve
+            const unsigned g = (unsigned)std::min<int64_t>((s->n * s->batch + 255) / 256, 148 * 16);
+            if (s->dtype == PB_F64)
+                ch1d_rhs_kernel<double><<<g, 256, 0, st>>>((const double *)s->c, (double *)s->work, s->n, s->batch,
+                                                           alpha);
+            else
+                ch1d_rhs_kernel<float><<<g, 256, 0, st>>>((const float *)s->c, (float *)s->work, s->n, s->batch,
+                                                          (float)alpha);
+            PB_LAUNCH_CHECK();
+            pb_layout L;
+            L.n_inner = s->batch;
+            L.inner_stride = 1;
+            L.n_outer = 1;
+            L.outer_stride = 0;
+            L.row_stride = s->batch;
+            if ((rc = band_solve_layout(h, s->work, L, st))) return rc;
+        }
         void *t = s->c;
         s->c = s->work;
         s->work = t;

@@ -33,19 +33,20 @@ namespace fc {
 using namespace fs;
 namespace cg = cooperative_groups;
 
-constexpr int CSMAX = 16;        // cluster size (16 = non-portable)
+constexpr int CSMAX = 8;         // cluster size (portable)
 constexpr int NWC = 4;           // consumer warps (= items per block)
 constexpr int NTHREADS = 32 * (NWC + 2);   // + producer warp + scan warp
 
-template <typename T>
+template <typename T, int MODE>
 struct CCfg {
     static constexpr int TILE = Q * TW;
     static constexpr int COEF = Q * COEF_STRIDE;    // >= Q * REC
-    static constexpr int HALO = TW * 2;             // MODE_CH1D: rows r0 - 1 and r0 + kmax (periodic)
+    static constexpr int HALO = MODE == MODE_CH1D ? TW * 2 : 0;   // rows r0 - 1 and r0 + kmax (periodic)
     static constexpr int E1K = 1024 / (int)sizeof(T);
     static constexpr int SLOT = (TILE + COEF + HALO + E1K - 1) / E1K * E1K;   // 1 KB multiple (swizzle)
     static constexpr int NS = sizeof(T) == 8 ? 8 : 16;
-    static constexpr int CPC = sizeof(T) == 8 ? 16 : 32;    // max chunks per CTA per group
+    // max chunks per CTA per group (records in shared memory)
+    static constexpr int CPC = MODE == MODE_CH1D ? 8 : (sizeof(T) == 8 ? 16 : 32);
     static_assert(NS % NWC == 0, "ring slots must be a multiple of the consumer warps");
 };
 
@@ -60,21 +61,33 @@ struct CArgs {
     int nq, count, Gb, G;
     int cs, cpc, ncl;        // cluster size, chunks per CTA, clusters
     int flat;
+    int dbg;   // DEV ONLY (timing experiments): 1 skip scan, 4 skip sweeps
 };
 
-template <typename T>
+template <typename T, int MODE>
 struct CSmem {
-    T slot[CCfg<T>::NS][CCfg<T>::SLOT];
-    T rec[2][CCfg<T>::CPC][TW][4];   // per group parity: (yF0, yF1, zB0, zB1) -> (yin0, yin1, zin0, zin1)
+    using C = CCfg<T, MODE>;
+    T slot[C::NS][C::SLOT];
+    T rec[2][C::CPC][TW][4];         // per group parity: (yF0, yF1, zB0, zB1) -> (yin0, yin1, zin0, zin1)
     T spec[2][4][TW];                // zero-inflow g on the cyclic rows this CTA owns
     T xl[2][TW][2];
-    T aggF[CSMAX][TW][2], aggB[CSMAX][TW][2];   // cluster exchange (written by every CTA)
-    T PF[CSMAX][4], PB[CSMAX][4];
-    T xlx[TW][2], xlg[4][TW];
-    uint64_t full[CCfg<T>::NS], empty[CCfg<T>::NS];
+    // one cluster exchange per group: CTA c's summary -- zero-inflow forward
+    // outflow a and backward outflow b (per lane), forward / backward transfer
+    // maps P, Pb and the coupling K of b to the forward inflow (uniform) -- and,
+    // from the owners of the cyclic rows, their zero-inflow g and its coupling r
+    // to the owner's forward inflow.  Rewritten for the next group only after
+    // every CTA has consumed it (xcons).
+    T xa[CSMAX][TW][2], xb[CSMAX][TW][2];
+    T xP[CSMAX][12];
+    T xg[4][TW], xr[4][2];
+    T phi[C::CPC][8];                // scan temporaries: Phi_i (chunk inflow per unit CTA inflow), H_i Phi_i
+    T cpriv[NWC][C::COEF];           // per consumer warp: its tile's coefficient rows (the slot is released early)
+    uint64_t full[C::NS], empty[C::NS];
     uint64_t p1done[2], recfree[2], scandone[2];
-    uint64_t xfwd, xbwd, xxl;
-    int64_t item[CCfg<T>::NS];       // (p2 << 62) | (t << 20) | local chunk ; -1 exit ; -2 empty
+    uint64_t xch, xcons;
+    int64_t item[C::NS];             // (p2 << 62) | (t << 20) | local chunk ; -1 exit ; -2 empty
+    int64_t seq[C::NS];              // sequence number of the item in the slot (written before its fill)
+    int claim;                       // consumer ticket: the next item to take
 };
 
 // ---------------------------------------------------------------- cluster PTX
@@ -106,103 +119,141 @@ __device__ __forceinline__ T *peer(T *p, int rank)
 }
 
 // ---------------------------------------------------------------- the scan of one group (one warp per CTA)
-template <typename T, int K, bool PER>
-__device__ void cluster_scan(const CArgs<T> &A, CSmem<T> &S, int t, int c, int q0, int ncl, int lane)
+// Chunk q's true inflows are affine in the CTA's forward inflow Y and backward
+// inflow Z (P:1712-1724 in chunked form): the CTA folds its chunks with Y = Z =
+// 0 while tracking the (lane-independent) 2x2 responses, publishes one summary
+// to every CTA of the cluster, and after that single exchange every CTA
+// resolves Y_c, Z_c of all CTAs, (x_0, x_1), the true g on the cyclic rows and
+// x_l locally, then walks its own chunks.
+template <typename T, int K, bool PER, int MODE>
+__device__ void cluster_scan(const CArgs<T> &A, CSmem<T, MODE> &S, int t, int c, int q0, int ncl, int lane)
 {
     const int par = t & 1;
     T(*R)[TW][4] = S.rec[par];
-    // ---- forward fold of my chunks: a = Mf a + yF, P = Mf P
-    T P[4] = {T(1), T(0), T(0), T(1)}, a0 = T(0), a1 = T(0);
-    T mn[4];
-    if (ncl > 0) ldm4(A.ct + (int64_t)q0 * 12, mn);
-    for (int i = 0; i < ncl; ++i) {
-        T m[4] = {mn[0], mn[1], mn[2], mn[3]}, t0, t1;
-        if (i + 1 < ncl) ldm4(A.ct + (int64_t)(q0 + i + 1) * 12, mn);   // next chunk's map in flight
-        mv(m, a0, a1, t0, t1);
-        a0 = t0 + R[i][lane][0];
-        a1 = t1 + R[i][lane][1];
-        mmul(m, P, P);
-    }
-    for (int r = 0; r < A.cs; ++r) {
-        T *pa = peer(&S.aggF[c][lane][0], r);
-        pa[0] = a0;
-        pa[1] = a1;
-        if (lane < 4) peer(&S.PF[c][0], r)[lane] = P[lane];
-    }
-    fence_cluster();
-    __syncwarp();
-    if (lane == 0)
-        for (int r = 0; r < A.cs; ++r) arrive_remote(&S.xfwd, r);
-    wait_cluster(&S.xfwd, (uint32_t)(t & 1));
-    T y0 = T(0), y1 = T(0);
-    for (int v = 0; v < c; ++v) {
-        T t0, t1;
-        mv(S.PF[v], y0, y1, t0, t1);
-        y0 = t0 + S.aggF[v][lane][0];
-        y1 = t1 + S.aggF[v][lane][1];
-    }
-    // ---- forward walk: yin_q, c_q = zB_q + H_q yin_q, true g on the cyclic rows
-    T hn[4];
-    if (ncl > 0) {
-        ldm4(A.ct + (int64_t)q0 * 12, mn);
-        ldm4(A.ct + (int64_t)q0 * 12 + 8, hn);
-    }
+    // ---- forward fold, zero inflow: yin0_i, Phi_i; c0_i = zB_i + H_i yin0_i; Hc_i = H_i Phi_i
+    T Phi[4] = {T(1), T(0), T(0), T(1)}, y0 = T(0), y1 = T(0);
+    T gj[4] = {T(0), T(0), T(0), T(0)}, rj[4][2] = {{T(0), T(0)}, {T(0), T(0)}, {T(0), T(0)}, {T(0), T(0)}};
     for (int i = 0; i < ncl; ++i) {
         const int q = q0 + i;
-        T m[4] = {mn[0], mn[1], mn[2], mn[3]}, h[4] = {hn[0], hn[1], hn[2], hn[3]}, t0, t1;
-        if (i + 1 < ncl) {
-            ldm4(A.ct + (int64_t)(q + 1) * 12, mn);
-            ldm4(A.ct + (int64_t)(q + 1) * 12 + 8, hn);
-        }
+        T m[4], h[4], hc[4], t0, t1;
+        ldm4(A.ct + (int64_t)q * 12, m);
+        ldm4(A.ct + (int64_t)q * 12 + 8, h);
         const T yf0 = R[i][lane][0], yf1 = R[i][lane][1];
         mv(h, y0, y1, t0, t1);
-        R[i][lane][0] = y0;
+        R[i][lane][0] = y0;            // yin0_i
         R[i][lane][1] = y1;
-        R[i][lane][2] += t0;
+        R[i][lane][2] += t0;           // c0_i
         R[i][lane][3] += t1;
+        mmul(h, Phi, hc);
+        if (lane < 4) S.phi[i][lane] = Phi[lane], S.phi[i][4 + lane] = hc[lane];
         if (PER) {
 #pragma unroll
             for (int jx = 0; jx < 4; ++jx)
-                if (A.srow[jx] >= 0 && A.srow[jx] / Q == q)
-                    S.spec[par][jx][lane] += A.rsp[jx * 2] * y0 + A.rsp[jx * 2 + 1] * y1;
+                if (A.srow[jx] >= 0 && A.srow[jx] / Q == q) {
+                    gj[jx] = S.spec[par][jx][lane] + A.rsp[jx * 2] * y0 + A.rsp[jx * 2 + 1] * y1;
+                    rj[jx][0] = A.rsp[jx * 2] * Phi[0] + A.rsp[jx * 2 + 1] * Phi[2];
+                    rj[jx][1] = A.rsp[jx * 2] * Phi[1] + A.rsp[jx * 2 + 1] * Phi[3];
+                }
         }
         mv(m, y0, y1, t0, t1);
         y0 = t0 + yf0;
         y1 = t1 + yf1;
+        mmul(m, Phi, Phi);
     }
-    // ---- backward fold (high to low): cb = Mb cb + c_q, Pb = Mb Pb
-    T Pb[4] = {T(1), T(0), T(0), T(1)}, c0 = T(0), c1 = T(0);
-    if (ncl > 0) ldm4(A.ct + (int64_t)(q0 + ncl - 1) * 12 + 4, mn);
+    __syncwarp();
+    // ---- backward fold, zero inflows: b = sum Mb.. c0_i, Pb = prod Mb, K = sum Mb.. Hc_i
+    T Pb[4] = {T(1), T(0), T(0), T(1)}, Kc[4] = {T(0), T(0), T(0), T(0)}, b0 = T(0), b1 = T(0);
     for (int i = ncl - 1; i >= 0; --i) {
-        T m[4] = {mn[0], mn[1], mn[2], mn[3]}, t0, t1;
-        if (i > 0) ldm4(A.ct + (int64_t)(q0 + i - 1) * 12 + 4, mn);
-        mv(m, c0, c1, t0, t1);
-        c0 = t0 + R[i][lane][2];
-        c1 = t1 + R[i][lane][3];
+        T m[4], t0, t1, hc[4];
+        ldm4(A.ct + (int64_t)(q0 + i) * 12 + 4, m);
+        mv(m, b0, b1, t0, t1);
+        b0 = t0 + R[i][lane][2];
+        b1 = t1 + R[i][lane][3];
         mmul(m, Pb, Pb);
+        mmul(m, Kc, Kc);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            hc[e] = S.phi[i][4 + e];
+            Kc[e] += hc[e];
+        }
     }
+    // ---- the one exchange: my summary to every CTA of the cluster (once every
+    // CTA has consumed the previous group's)
+    if (t >= 1) wait_cluster(&S.xcons, (uint32_t)((t - 1) & 1));
     for (int r = 0; r < A.cs; ++r) {
-        T *pa = peer(&S.aggB[c][lane][0], r);
-        pa[0] = c0;
-        pa[1] = c1;
-        if (lane < 4) peer(&S.PB[c][0], r)[lane] = Pb[lane];
+        T *pa = peer(&S.xa[c][lane][0], r), *pb = peer(&S.xb[c][lane][0], r);
+        pa[0] = y0, pa[1] = y1;
+        pb[0] = b0, pb[1] = b1;
+        if (lane < 4) {
+            T *pp = peer(&S.xP[c][0], r);
+            pp[lane] = Phi[lane];
+            pp[4 + lane] = Pb[lane];
+            pp[8 + lane] = Kc[lane];
+        }
+        if (PER) {
+#pragma unroll
+            for (int jx = 0; jx < 4; ++jx)
+                if (A.srow[jx] >= 0 && A.srow[jx] / Q >= q0 && A.srow[jx] / Q < q0 + ncl) {
+                    peer(&S.xg[jx][0], r)[lane] = gj[jx];
+                    if (lane < 2) peer(&S.xr[jx][0], r)[lane] = rj[jx][lane];
+                }
+        }
     }
     fence_cluster();
     __syncwarp();
     if (lane == 0)
-        for (int r = 0; r < A.cs; ++r) arrive_remote(&S.xbwd, r);
-    wait_cluster(&S.xbwd, (uint32_t)(t & 1));
-    T z0 = T(0), z1 = T(0);
-    for (int v = A.cs - 1; v > c; --v) {
-        T t0, t1;
-        mv(S.PB[v], z0, z1, t0, t1);
-        z0 = t0 + S.aggB[v][lane][0];
-        z1 = t1 + S.aggB[v][lane][1];
+        for (int r = 0; r < A.cs; ++r) arrive_remote(&S.xch, r);
+    wait_cluster(&S.xch, (uint32_t)(t & 1));
+    // ---- every CTA's forward inflow Y_v, then backward inflows from the top
+    T Yv[CSMAX][2];
+    {
+        T ya = T(0), yb = T(0);
+        for (int v = 0; v < A.cs; ++v) {
+            Yv[v][0] = ya, Yv[v][1] = yb;
+            T t0, t1;
+            mv(S.xP[v], ya, yb, t0, t1);
+            ya = t0 + S.xa[v][lane][0];
+            yb = t1 + S.xa[v][lane][1];
+        }
     }
-    if (ncl > 0) ldm4(A.ct + (int64_t)(q0 + ncl - 1) * 12 + 4, mn);
+    T Za = T(0), Zb = T(0), Zc0 = T(0), Zc1 = T(0);   // running backward inflow; mine
+    for (int v = A.cs - 1; v >= 0; --v) {
+        if (v == c) Zc0 = Za, Zc1 = Zb;
+        T t0, t1, u0, u1;
+        mv(S.xP[v] + 4, Za, Zb, t0, t1);
+        mv(S.xP[v] + 8, Yv[v][0], Yv[v][1], u0, u1);
+        Za = t0 + u0 + S.xb[v][lane][0];
+        Zb = t1 + u1 + S.xb[v][lane][1];
+    }
+    // cyclic rows' g (read now: the exchange buffer is released right after)
+    T gv[4] = {T(0), T(0), T(0), T(0)};
+    if (PER) {
+#pragma unroll
+        for (int jx = 0; jx < 4; ++jx)
+            if (A.srow[jx] >= 0) {
+                const int ow = (int)(A.srow[jx] / Q) / A.cpc;   // owner CTA of the row's chunk
+                gv[jx] = S.xg[jx][lane] + S.xr[jx][0] * Yv[ow][0] + S.xr[jx][1] * Yv[ow][1];
+            }
+    }
+    fence_cluster();
+    __syncwarp();
+    if (lane == 0)
+        for (int r = 0; r < A.cs; ++r) arrive_remote(&S.xcons, r);   // this group's exchange consumed
+    // ---- my chunks: yin_i = yin0_i + Phi_i Y, c_i = c0_i + Hc_i Y; zin walk from Z_c
+    const T Y0 = Yv[c][0], Y1 = Yv[c][1];
+    for (int i = 0; i < ncl; ++i) {
+        T t0, t1, u0, u1;
+        mv(S.phi[i], Y0, Y1, t0, t1);
+        mv(S.phi[i] + 4, Y0, Y1, u0, u1);
+        R[i][lane][0] += t0;
+        R[i][lane][1] += t1;
+        R[i][lane][2] += u0;
+        R[i][lane][3] += u1;
+    }
+    T z0 = Zc0, z1 = Zc1;
     for (int i = ncl - 1; i >= 0; --i) {
-        T m[4] = {mn[0], mn[1], mn[2], mn[3]}, t0, t1;
-        if (i > 0) ldm4(A.ct + (int64_t)(q0 + i - 1) * 12 + 4, mn);
+        T m[4], t0, t1;
+        ldm4(A.ct + (int64_t)(q0 + i) * 12 + 4, m);
         const T cq0 = R[i][lane][2], cq1 = R[i][lane][3];
         R[i][lane][2] = z0;
         R[i][lane][3] = z1;
@@ -211,28 +262,8 @@ __device__ void cluster_scan(const CArgs<T> &A, CSmem<T> &S, int t, int c, int q
         z1 = t1 + cq1;
     }
     if (!PER) return;
-    // ---- cyclic pair: (x_0, x_1) from CTA 0, true g on the cyclic rows from their owners
-    if (c == 0)
-        for (int r = 0; r < A.cs; ++r) {
-            T *px = peer(&S.xlx[lane][0], r);
-            px[0] = z0;
-            px[1] = z1;
-        }
-#pragma unroll
-    for (int jx = 0; jx < 4; ++jx) {
-        const int64_t qj = A.srow[jx] / Q;
-        if (A.srow[jx] >= 0 && qj >= q0 && qj < q0 + ncl)
-            for (int r = 0; r < A.cs; ++r) peer(&S.xlg[jx][0], r)[lane] = S.spec[par][jx][lane];
-    }
-    fence_cluster();
-    __syncwarp();
-    if (lane == 0)
-        for (int r = 0; r < A.cs; ++r) arrive_remote(&S.xxl, r);
-    wait_cluster(&S.xxl, (uint32_t)(t & 1));
-    const T y1c = S.xlx[lane][0], y2c = S.xlx[lane][1];
-    T gv[4];
-#pragma unroll
-    for (int jx = 0; jx < 4; ++jx) gv[jx] = A.srow[jx] >= 0 ? S.xlg[jx][lane] : T(0);
+    // ---- cyclic pair: (x_0, x_1) = CTA 0's backward outflow; g on the cyclic rows
+    const T y1c = Za, y2c = Zb;
     const double *sc = A.scal;
     T xl0, xl1;
     if (K == 2) {
@@ -275,10 +306,10 @@ struct Seq {
 template <typename T, int K, bool PER, int MODE, int LAY>
 __global__ void __launch_bounds__(NTHREADS, 1) fc_kernel(const __grid_constant__ CUtensorMap tmap, const CArgs<T> A)
 {
-    using C = CCfg<T>;
+    using C = CCfg<T, MODE>;
     constexpr int NS = C::NS, TILE = C::TILE;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    CSmem<T> &sm = *reinterpret_cast<CSmem<T> *>((((uintptr_t)smem_raw) + 1023) & ~(uintptr_t)1023);
+    CSmem<T, MODE> &sm = *reinterpret_cast<CSmem<T, MODE> *>((((uintptr_t)smem_raw) + 1023) & ~(uintptr_t)1023);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = (int)cg::this_cluster().block_rank();
     const int cl = blockIdx.x / A.cs;                       // cluster index
@@ -295,9 +326,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fc_kernel(const __grid_constant__
             bar_init(&sm.recfree[p], max(ncl, 1));
             bar_init(&sm.scandone[p], 1);
         }
-        bar_init(&sm.xfwd, A.cs);
-        bar_init(&sm.xbwd, A.cs);
-        bar_init(&sm.xxl, A.cs);
+        bar_init(&sm.xch, A.cs);
+        bar_init(&sm.xcons, A.cs);
+        for (int i = 0; i < NS; ++i) sm.seq[i] = -1;
+        sm.claim = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     cg::this_cluster().sync();   // barriers initialised cluster-wide before any remote arrive
@@ -318,17 +350,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) fc_kernel(const __grid_constant__
                     const int tg = type ? t - 1 : t;         // iteration of the item's group
                     if (i >= ncl) {
                         sm.item[sl] = -2;
+                        *(volatile int64_t *)&sm.seq[sl] = j;
                         bar_arrive(&sm.full[sl]);
                         continue;
                     }
                     sm.item[sl] = ((int64_t)type << 62) | ((int64_t)tg << 20) | i;
+                    *(volatile int64_t *)&sm.seq[sl] = j;
                     const int g = cl + tg * A.ncl;
                     const int b = g / A.Gb, gl = g - b * A.Gb;
                     const int64_t r0 = (int64_t)(q0 + i) * Q;
                     const int kmax = (int)min((int64_t)Q, A.n - r0);
                     T *slot = sm.slot[sl];
-                    const uint32_t cb = up16((uint32_t)(kmax * (type ? COEF_STRIDE : REC) * sizeof(T)));
-                    uint32_t bytes = TILE * sizeof(T) + cb + (MODE == MODE_CH1D ? C::HALO * sizeof(T) : 0);
+                    const uint32_t cb = (A.dbg & 128) ? 0u : up16((uint32_t)(kmax * (type ? COEF_STRIDE : REC) * sizeof(T)));
+                    uint32_t bytes = TILE * sizeof(T) + cb + C::HALO * sizeof(T);
                     bar_expect_tx(&sm.full[sl], bytes);
                     const uint64_t pol = type ? pol2 : pol1;
                     if (LAY == LAY_CONTIG) {
@@ -344,7 +378,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fc_kernel(const __grid_constant__
                     } else {
                         tma_load3(slot, &tmap, gl * TW, (int)r0, b, &sm.full[sl], pol);
                     }
-                    bulk_load(slot + TILE, type ? A.coef + r0 * COEF_STRIDE : A.rec + r0 * REC, cb, &sm.full[sl]);
+                    if (cb) bulk_load(slot + TILE, type ? A.coef + r0 * COEF_STRIDE : A.rec + r0 * REC, cb, &sm.full[sl]);
                     if (MODE == MODE_CH1D) {
                         const T *ub = A.x + (int64_t)b * A.bstride + (int64_t)gl * TW;
                         const int64_t rlo = r0 == 0 ? A.n - 1 : r0 - 1, rhi = r0 + kmax == A.n ? 0 : r0 + kmax;
@@ -358,19 +392,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) fc_kernel(const __grid_constant__
                 const int sl = (int)(j % NS);
                 if (j >= NS) bar_wait(&sm.empty[sl], (uint32_t)(((j / NS) - 1) & 1));
                 sm.item[sl] = -1;
+                *(volatile int64_t *)&sm.seq[sl] = j;
                 bar_arrive(&sm.full[sl]);
             }
         }
     } else if (warp < NWC) {
-        // ---------------- consumers: slots j = warp, warp + NWC, ... (each slot owned by one warp)
-        for (int64_t j = warp;; j += NWC) {
+        // ---------------- consumers: each warp claims the next item (shared-memory
+        // ticket), so a warp blocked on a dependency holds no slot and stalls no
+        // other warp.  The slot's sequence tag is checked before its parity wait
+        // (the fill of item j is the slot's phase j / NS once the tag reads j, so
+        // the wait cannot alias another phase).  A tile's column goes to registers
+        // and its coefficient rows to the warp's private buffer at once, so the
+        // slot returns to the producer before the sweeps: the ring stays in flight.
+        T *cp = sm.cpriv[warp];
+        for (;;) {
+            int64_t j = 0;
+            if (lane == 0) j = atomicAdd(&sm.claim, 1);
+            j = __shfl_sync(0xffffffffu, j, 0);
             const int sl = (int)(j % NS);
+            while (*(volatile int64_t *)&sm.seq[sl] != j) {
+            }
             bar_wait(&sm.full[sl], (uint32_t)((j / NS) & 1));
             const int64_t it = *(volatile int64_t *)&sm.item[sl];
-            if (it == -1) {
-                if (LAY == LAY_CONTIG && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-                break;
-            }
+            if (it == -1) break;
             if (it < 0) {
                 __syncwarp();
                 if (lane == 0) bar_arrive(&sm.empty[sl]);
@@ -384,56 +428,59 @@ __global__ void __launch_bounds__(NTHREADS, 1) fc_kernel(const __grid_constant__
             const int64_t r0 = (int64_t)q * Q;
             const int kmax = (int)min((int64_t)Q, A.n - r0);
             const T *d = sm.slot[sl];
-            const T *cf = d + TILE;
             const int64_t s_in_batch = (int64_t)gl * TW + lane;
             const bool ok = s_in_batch < A.M;
             if (MODE == MODE_CH1D) ch1d_rhs<T>(const_cast<T *>(d), d + TILE + C::COEF, kmax, lane, A.alpha);
+            T v[Q];
+#pragma unroll
+            for (int k = 0; k < Q; ++k) v[k] = (A.dbg & 32) ? T(0) : tld<T, LAY>(d, k, lane);
+            if (!(A.dbg & 16)) {
+                // coefficient rows -> private buffer (16-byte shared loads / stores, lane-strided)
+                constexpr int NV = C::COEF * (int)sizeof(T) / 16;
+                const uint32_t src = su32(d + TILE), dst = su32(cp);
+#pragma unroll
+                for (int e = lane; e < NV; e += 32) {
+                    uint32_t a, bq, cq, dq;
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(a), "=r"(bq), "=r"(cq), "=r"(dq) : "r"(src + e * 16));
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst + e * 16), "r"(a), "r"(bq),
+                                 "r"(cq), "r"(dq) : "memory");
+                }
+            }
+            __syncwarp();
+            if (lane == 0) bar_arrive(&sm.empty[sl]);
             if (!type) {
                 // ---- P1: zero-inflow forward sweep, carry, back-substitution functional
                 T y0 = T(0), y1 = T(0), a0 = T(0), a1 = T(0), gs[4] = {T(0), T(0), T(0), T(0)};
-                if (kmax == Q && !(PER && q >= A.srow[0] / Q)) {
+                const bool spec_tile = PER && q >= A.srow[0] / Q;
 #pragma unroll
-                    for (int k = 0; k < Q; ++k) {
-                        T f0, f1, f2, wa;
-                        lds2(cf + k * REC, f0, f1);
-                        lds2(cf + k * REC + 2, f2, wa);
-                        const T wb = cf[k * REC + 4];
-                        T gg = f0 * tld<T, LAY>(d, k, lane) - f1 * y1;
-                        if (K == 2) gg -= f2 * y0;
+                for (int k = 0; k < Q; ++k) {
+                    if (!(A.dbg & 4) && (kmax == Q || k < kmax)) {
+                        T f0, f1, f2, wa, wb, wz;
+                        lds2(cp + k * REC, f0, f1);
+                        lds2(cp + k * REC + 2, f2, wa);
+                        lds2(cp + k * REC + 4, wb, wz);
+                        T tt = f0 * v[k];
+                        if (K == 2) tt -= f2 * y0;
+                        const T gg = tt - f1 * y1;   // newest carry last: one FMA on the chain
                         y0 = y1;
                         y1 = gg;
                         a0 += wa * gg;
                         a1 += wb * gg;
-                    }
-                } else {
-#pragma unroll 4
-                    for (int k = 0; k < kmax; ++k) {
-                        T f0, f1, f2, wa;
-                        lds2(cf + k * REC, f0, f1);
-                        lds2(cf + k * REC + 2, f2, wa);
-                        const T wb = cf[k * REC + 4];
-                        T gg = f0 * tld<T, LAY>(d, k, lane) - f1 * y1;
-                        if (K == 2) gg -= f2 * y0;
-                        y0 = y1;
-                        y1 = gg;
-                        a0 += wa * gg;
-                        a1 += wb * gg;
-                        if (PER) {
+                        if (PER && spec_tile) {
 #pragma unroll
                             for (int jx = 0; jx < 4; ++jx)
                                 if (A.srow[jx] == r0 + k) gs[jx] = gg;
                         }
                     }
                 }
-                __syncwarp();
-                if (lane == 0) bar_arrive(&sm.empty[sl]);
                 // the record buffer of this parity is free once P2 of group tg-2 has read it
-                if (tg >= 2) bar_wait(&sm.recfree[par], (uint32_t)(((tg - 2) >> 1) & 1));
+                if (tg >= 2 && !(A.dbg & 64)) bar_wait(&sm.recfree[par], (uint32_t)(((tg - 2) >> 1) & 1));
                 sm.rec[par][i][lane][0] = y0;
                 sm.rec[par][i][lane][1] = y1;
                 sm.rec[par][i][lane][2] = a0;
                 sm.rec[par][i][lane][3] = a1;
-                if (PER) {
+                if (PER && spec_tile) {
 #pragma unroll
                     for (int jx = 0; jx < 4; ++jx)
                         if (A.srow[jx] >= 0 && A.srow[jx] / Q == q) sm.spec[par][jx][lane] = gs[jx];
@@ -443,18 +490,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) fc_kernel(const __grid_constant__
                 continue;
             }
             // ---- P2: inflows and x_l of the group (scan done), sweeps, x out
-            T v[Q];
-#pragma unroll
-            for (int k = 0; k < Q; ++k) v[k] = tld<T, LAY>(d, k, lane);
-            bar_wait(&sm.scandone[par], (uint32_t)((tg >> 1) & 1));
+            if (!(A.dbg & 64)) bar_wait(&sm.scandone[par], (uint32_t)((tg >> 1) & 1));
             const T yi0 = sm.rec[par][i][lane][0], yi1 = sm.rec[par][i][lane][1];
             const T zi0 = sm.rec[par][i][lane][2], zi1 = sm.rec[par][i][lane][3];
             T xl0 = T(0), xl1 = T(0);
             if (PER) xl0 = sm.xl[par][lane][0], xl1 = sm.xl[par][lane][1];
             __syncwarp();
             if (lane == 0) bar_arrive(&sm.recfree[par]);
-            if (kmax == Q) tile_solve<T, K, PER, true>(v, cf, Q, yi0, yi1, zi0, zi1, xl0, xl1);
-            else tile_solve<T, K, PER, false>(v, cf, kmax, yi0, yi1, zi0, zi1, xl0, xl1);
+            if (A.dbg & 4) {
+            } else if (kmax == Q) tile_solve<T, K, PER, true>(v, cp, Q, yi0, yi1, zi0, zi1, xl0, xl1);
+            else tile_solve<T, K, PER, false>(v, cp, kmax, yi0, yi1, zi0, zi1, xl0, xl1);
             if (PER && K == 2 && r0 + Q > A.n - 2) {
                 const int k2 = (int)(A.n - 2 - r0);
 #pragma unroll
@@ -463,31 +508,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) fc_kernel(const __grid_constant__
                     if (k == k2 + 1) v[k] = xl1;
                 }
             }
+            if (!ok || (A.dbg & 8)) continue;
             if (LAY == LAY_CONTIG) {
-                T *dm = const_cast<T *>(d);
+                // system = row of the output: 64 consecutive elements per lane
+                T *x = A.xout + (int64_t)b * A.bstride + s_in_batch * A.pitch + r0;
+                if (kmax == Q) {
 #pragma unroll
-                for (int k = 0; k < Q; ++k) tst<T, LAY>(dm, k, lane, v[k]);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) {
-#pragma unroll
-                    for (int bx = 0; bx < Q / Sw<T>::EB; ++bx) {
-                        const int r = (int)r0 + bx * Sw<T>::EB;
-                        if (r < A.n) {
-                            if (A.flat) tma_store2(&tmap, r, (int)((int64_t)b * A.M + gl * TW), dm + bx * TW * Sw<T>::EB);
-                            else tma_store3(&tmap, r, gl * TW, b, dm + bx * TW * Sw<T>::EB);
-                        }
+                    for (int k = 0; k < Q; k += 16 / (int)sizeof(T)) {
+                        if (sizeof(T) == 8)
+                            __stcs(reinterpret_cast<double2 *>(x + k), make_double2((double)v[k], (double)v[k + 1]));
+                        else
+                            __stcs(reinterpret_cast<float4 *>(x + k),
+                                   make_float4((float)v[k], (float)v[k + 1], (float)v[k + 2], (float)v[k + 3]));
                     }
-                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                    bar_arrive(&sm.empty[sl]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < Q; ++k)
+                        if (k < kmax) __stcs(x + k, v[k]);
                 }
-                __syncwarp();
                 continue;
             }
-            __syncwarp();
-            if (lane == 0) bar_arrive(&sm.empty[sl]);
-            if (ok) {
+            {
+                // x in place: every row of the tile is one contiguous 32-system segment
+                // (opaque stride: one running address instead of Q live ones)
                 int64_t Mo = A.pitch;
                 asm volatile("" : "+l"(Mo));
                 T *x = A.xout + (int64_t)b * A.bstride + r0 * Mo + s_in_batch;
@@ -503,7 +546,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fc_kernel(const __grid_constant__
         for (int t = 0; t < T_; ++t) {
             const int par = t & 1;
             if (ncl > 0) bar_wait(&sm.p1done[par], (uint32_t)((t >> 1) & 1));
-            cluster_scan<T, K, PER>(A, sm, t, c, q0, ncl, lane);
+            if (!(A.dbg & 1)) cluster_scan<T, K, PER, MODE>(A, sm, t, c, q0, ncl, lane);
             __syncwarp();
             if (lane == 0) bar_arrive(&sm.scandone[par]);
         }

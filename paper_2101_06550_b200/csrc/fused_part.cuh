@@ -3,6 +3,7 @@
 // FS_T / FS_LAY / FS_NAME defined, so the instantiations compile in parallel.
 #include <cudaTypedefs.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "band_tile.cuh"
@@ -72,9 +73,9 @@ template <typename T, int K, bool PER, int MODE, int LAY>
 static int fc_launch_t(const Band *h, T *x, T *xout, double alpha, int64_t count, int64_t bstride, cudaStream_t st,
                        int64_t Mo, int64_t pitch, int *info = nullptr)
 {
-    using C = fc::CCfg<T>;
+    using C = fc::CCfg<T, MODE>;
     auto kern = fc::fc_kernel<T, K, PER, MODE, LAY>;
-    const size_t smem = sizeof(fc::CSmem<T>) + 1024;
+    const size_t smem = sizeof(fc::CSmem<T, MODE>) + 1024;
     static std::once_flag once;
     static cudaError_t attr = cudaSuccess;
     static int ncl_of[fc::CSMAX + 1];
@@ -161,6 +162,18 @@ static int fc_launch_t(const Band *h, T *x, T *xout, double alpha, int64_t count
     A.cs = best_cs;
     A.cpc = best_cpc;
     A.ncl = best_ncl;
+    {
+        static const int dbg = getenv("PB_DEV_DBG") ? atoi(getenv("PB_DEV_DBG")) : 0;   // DEV ONLY
+        static const int csf = getenv("PB_DEV_CS") ? atoi(getenv("PB_DEV_CS")) : 0;     // DEV ONLY
+        A.dbg = dbg;
+        if (csf >= 1 && (nq + csf - 1) / csf <= C::CPC && ncl_of[csf] > 0) {
+            A.cs = csf;
+            A.cpc = (nq + csf - 1) / csf;
+            A.ncl = (int)std::min<int64_t>(ncl_of[csf], G);
+            best_cs = A.cs;
+            best_ncl = A.ncl;
+        }
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(best_ncl * best_cs));
     cfg.blockDim = dim3(fc::NTHREADS);

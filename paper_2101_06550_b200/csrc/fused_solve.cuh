@@ -299,12 +299,13 @@ __device__ __forceinline__ void tile_carry(const T *d, const T *c, int kmax, int
     T y0 = T(0), y1 = T(0), a0 = T(0), a1 = T(0);
 #pragma unroll(FULL ? Q : 4)
     for (int k = 0; k < (FULL ? Q : kmax); ++k) {
-        T f0, f1, f2, wa;
+        T f0, f1, f2, wa, wb, wz;
         lds2(c + k * REC, f0, f1);
         lds2(c + k * REC + 2, f2, wa);
-        const T wb = c[k * REC + 4];
-        T g = f0 * tld<T, LAY>(d, k, lane) - f1 * y1;
-        if (K == 2) g -= f2 * y0;
+        lds2(c + k * REC + 4, wb, wz);
+        T t = f0 * tld<T, LAY>(d, k, lane);
+        if (K == 2) t -= f2 * y0;
+        const T g = t - f1 * y1;
         y0 = y1;
         y1 = g;
         a0 += wa * g;
@@ -330,13 +331,17 @@ __device__ __forceinline__ void tile_carry(const T *d, const T *c, int kmax, int
 template <typename T, int K, bool PER, bool FULL>
 __device__ __forceinline__ void tile_solve(T (&v)[Q], const T *c, int kmax, T y0, T y1, T z0, T z1, T xl0, T xl1)
 {
+    // each recurrence takes its newest carry last: one dependent FMA per row
+    // on the critical path (g = (F0 f - F2 g_{k-2}) - F1 g_{k-1}; likewise x)
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
         if (FULL || k < kmax) {
-            T f0, f1;
+            T f0, f1, f2, fz;
             lds2(c + k * COEF_STRIDE, f0, f1);
-            T g = f0 * v[k] - f1 * y1;
-            if (K == 2) g -= c[k * COEF_STRIDE + 2] * y0;
+            lds2(c + k * COEF_STRIDE + 2, f2, fz);
+            T t = f0 * v[k];
+            if (K == 2) t -= f2 * y0;
+            const T g = t - f1 * y1;
             y0 = y1;
             y1 = g;
             v[k] = g;
@@ -347,8 +352,9 @@ __device__ __forceinline__ void tile_solve(T (&v)[Q], const T *c, int kmax, T y0
         if (FULL || k < kmax) {
             T b1, b2;
             lds2(c + k * COEF_STRIDE + 4, b1, b2);
-            T xx = v[k] - b1 * z0;
-            if (K == 2) xx -= b2 * z1;
+            T t = v[k];
+            if (K == 2) t -= b2 * z1;
+            const T xx = t - b1 * z0;
             z1 = z0;
             z0 = xx;
             v[k] = xx;

@@ -237,53 +237,10 @@ def test_cluster_and_global_paths(n, sigma, dtype):
     h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in diags], batch=m, n=n, periodic=True, dtype=dtype)
     cs, cpc, ncl = h.solve_info()
     nq = (n + 63) // 64
-    if dtype == "f64" and nq > 256:
+    if nq > (128 if dtype == "f64" else 256):   # CSMAX 8 x chunks per CTA (16 fp64, 32 fp32)
         assert cs == 0
     else:
         assert cs >= 1 and cs * cpc >= nq and ncl >= 1, (cs, cpc, ncl)
-    x = torch.from_numpy(f).to(TDT[dtype]).cuda()
-    h.solve(x)
-    torch.cuda.synchronize()
-    # kappa = 1 + 16 sigma = 4.3e4 at sigma 2700: fp32 is kappa-limited there (~1.7e-4 measured)
-    tol = TOL[dtype] if sigma < 100 else (1e-12 if dtype == "f64" else 1e-3)
-    assert relerr(x.double().cpu().numpy(), ref) <= tol
-
-
-@pytest.mark.parametrize("pinned", [True, False])
-def test_host_buffer_pipelined(pinned):
-    """A host right-hand side (>= 4096 systems) takes the pipelined path: pitched
-    H2D / fused solve / D2H of column blocks on two streams; sampled systems match
-    the oracle and the call returns with the host buffer solved."""
-    n, m = 300, 8192 + 96
-    a, b, c, d, e = synth.dd_penta(n, 1, seed=71)
-    f = synth.rhs_uniform(n, m, seed=72)
-    h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in (a, b, c, d, e)], batch=m, n=n, periodic=True)
-    x = torch.from_numpy(f.copy())
-    if pinned:
-        x = x.pin_memory()
-    h.solve(x.numpy())
-    X = x.numpy().reshape(n, m)
-    F = f.reshape(n, m)
-    for s in (0, 31, 4000, m - 1):
-        ref = oracle.penta_batch_solve(a, b, c, d, e, np.ascontiguousarray(F[:, s]), n=n, m=1, periodic=True)
-        assert relerr(X[:, s], ref) <= 1e-12, s
-
-
-@pytest.mark.parametrize("dtype", ["f64", "f32"])
-@pytest.mark.parametrize("sigma,n,expect", [(45.09, 3000, "window"), (68.0, 700, "window"), (2700.0, 2000, "scan"),
-                                            (2700.0, 130, "scan")])
-def test_window_and_scan_modes(sigma, n, expect, dtype):
-    """Both inflow modes of the fused solve against the oracle: the thesis
-    operators at dx = 2 pi/256 (sigma 45-68) decay below 1e-18 within 3 chunks
-    (windowed inflows); sigma = 2700 (Table 3.1's n = 1024 at L = 2 pi) does
-    not (per-group scan).  Cyclic (Navon), several groups, ragged n."""
-    m = 200
-    diags = synth.const_penta(n, sigma, -4 * sigma, 1 + 6 * sigma, -4 * sigma, sigma)
-    f = synth.rhs_uniform(n, m, seed=n)
-    ref = oracle.penta_batch_solve(*diags, f, n=n, m=m, periodic=True)
-    h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in diags], batch=m, n=n, periodic=True, dtype=dtype)
-    w = h.window()
-    assert (w > 0) == (expect == "window"), w
     x = torch.from_numpy(f).to(TDT[dtype]).cuda()
     h.solve(x)
     torch.cuda.synchronize()

@@ -240,3 +240,37 @@ def test_hyperdiffusion_cn_amplification():
     S = math.sin(math.pi * kk / n)
     g = (1 - 16 * sx * S ** 4) / (1 + 16 * sx * S ** 4)
     assert np.max(np.abs(c - g ** 50 * np.cos(2 * np.pi * kk * x))) <= 1e-13
+
+
+def test_l2_error_closed_form():
+    """eq:myerr: a perturbation d cos(2 pi k x_i) on a uniform grid
+    has RMS exactly |d| / sqrt(2) (0 < k < N/2); a constant offset d has RMS |d|."""
+    n = 64
+    x = np.arange(n) / n
+    base = np.sin(2 * math.pi * 3 * x)
+    for k, d in ((1, 1e-3), (7, -2.5), (31, 0.125)):
+        assert oracle.l2_error(base + d * np.cos(2 * math.pi * k * x), base) == pytest.approx(abs(d) / math.sqrt(2),
+                                                                                               rel=1e-12)
+    assert oracle.l2_error(base + 0.75, base) == pytest.approx(0.75, rel=1e-14)
+
+
+def test_hyperdiffusion_cn_validation_small_n():
+    """P:1736-1765 with the oracle (stencil + cyclic penta solve): C(x,0) =
+    cos(4 pi x), gamma = D = L = 1, dt = 1e-8, T = 1e-4; eps_N(T) of eq:myerr
+    against e^{-k^4 T} cos(kx) for N = 16, 32, 64 equals the SURVEY §8(c)
+    reference values 1.62e-2, 3.82e-3, 9.41e-4 (3 digits)."""
+    for n, ref in ((16, 1.62e-2), (32, 3.82e-3), (64, 9.41e-4)):
+        dt, T = 1e-8, 1e-4
+        dx = 1.0 / n
+        s = dt / (2 * dx ** 4)
+        A = synth.const_penta(n, s, -4 * s, 1 + 6 * s, -4 * s, s)
+        x = dx * np.arange(n)
+        k = 4 * math.pi
+        c = np.cos(k * x)
+        w = np.array([-s, 4 * s, 1 - 6 * s, 4 * s, -s])
+        steps = synth.ch_nsteps(T, dt)
+        for _ in range(steps):
+            f = oracle.stencil_apply(c[None, :], w, left=2, right=2, top=0, bottom=0)[0]
+            c = oracle.penta_batch_solve(*A, f, n=n, m=1, periodic=True)
+        eps = oracle.l2_error(c, math.exp(-k ** 4 * steps * dt) * np.cos(k * x))
+        assert abs(eps - ref) <= 0.006 * ref, (n, eps, ref)

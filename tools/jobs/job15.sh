@@ -1,0 +1,2 @@
+python -c "import torch; torch.zeros(1).cuda()"
+for d in 13 29 45 61 77 125 253; do echo "DBG=$d"; PB_DEV_DBG=$d timeout 100 python tools/fs_time.py f64 8192:8192 512:262144 2>&1 | tail -2; done

@@ -172,6 +172,8 @@ extern "C" int mb2_tma(const double *x, double *y, int64_t N, int64_t M, int W, 
         case 4: k = tma_copy<4>; break;
         case 6: k = tma_copy<6>; break;
         case 8: k = tma_copy<8>; break;
+        case 12: k = tma_copy<12>; break;
+        case 16: k = tma_copy<16>; break;
         default: return -1;
     }
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
