@@ -187,9 +187,10 @@ class PentaHandle(_Banded):
         return rhs
 
     def solve_info(self, layout="interleaved"):
-        """pent_solve_info: (cluster size, chunks per CTA, clusters) of the fused
-        solve; cluster size 0 = global-scan kernel, -1 = no fused plan."""
-        w = (ctypes.c_int * 3)()
+        """pent_solve_info: (cluster size, chunks per CTA, clusters, kernel) of the
+        fused solve; kernel 2 = tiles held on chip (one HBM pass), 1 = two-pass
+        cluster kernel, 0 = global-scan kernel; all -1 = no fused plan."""
+        w = (ctypes.c_int * 4)()
         _check(lib().pent_solve_info(self._h, _layout(layout), w))
         return tuple(w)
 

@@ -18,7 +18,7 @@ FLAGS = [
     "--expt-relaxed-constexpr",
     "-cudart", "static",
     "-I", os.path.join(ROOT, "include"),
-]
+] + os.environ.get("PB_EXTRA_NVCC_FLAGS", "").split()   # dev experiments only
 
 
 def _objs_stale() -> bool:

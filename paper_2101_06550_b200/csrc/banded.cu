@@ -923,7 +923,7 @@ int pent_solve_info(pb_penta_t h, int layout, int *info)
 {
     if (!h || !info || (layout != PB_INTERLEAVED && layout != PB_CONTIGUOUS))
         return pb::set_error(PB_EINVAL, "bad argument");
-    info[0] = info[1] = info[2] = -1;
+    info[0] = info[1] = info[2] = info[3] = -1;
     if (!h->shared() || !h->fplan.ok || h->seq_only) return PB_OK;
     return pb::fused_info(h, layout, h->batch, 1, info);
 }

@@ -62,11 +62,13 @@ struct CArgs {
     int cs, cpc, ncl;        // cluster size, chunks per CTA, clusters
     int flat;
     int dbg;   // DEV ONLY (timing experiments): 1 skip scan, 4 skip sweeps
+    long long *prof;   // DEV ONLY (FH_PROF builds)
 };
 
 template <typename T, int MODE>
 struct CSmem {
     using C = CCfg<T, MODE>;
+    static constexpr int NPAR = 2;   // record parities
     T slot[C::NS][C::SLOT];
     T rec[2][C::CPC][TW][4];         // per group parity: (yF0, yF1, zB0, zB1) -> (yin0, yin1, zin0, zin1)
     T spec[2][4][TW];                // zero-inflow g on the cyclic rows this CTA owns
@@ -78,6 +80,7 @@ struct CSmem {
     // to the owner's forward inflow.  Rewritten for the next group only after
     // every CTA has consumed it (xcons).
     T xa[CSMAX][TW][2], xb[CSMAX][TW][2];
+    T yv[CSMAX][TW][2];              // scan temporaries: every CTA's forward inflow
     T xP[CSMAX][12];
     T xg[4][TW], xr[4][2];
     T phi[C::CPC][8];                // scan temporaries: Phi_i (chunk inflow per unit CTA inflow), H_i Phi_i
@@ -124,136 +127,188 @@ __device__ __forceinline__ T *peer(T *p, int rank)
 // 0 while tracking the (lane-independent) 2x2 responses, publishes one summary
 // to every CTA of the cluster, and after that single exchange every CTA
 // resolves Y_c, Z_c of all CTAs, (x_0, x_1), the true g on the cyclic rows and
-// x_l locally, then walks its own chunks.
-template <typename T, int K, bool PER, int MODE>
-__device__ void cluster_scan(const CArgs<T> &A, CSmem<T, MODE> &S, int t, int c, int q0, int ncl, int lane)
+// x_l locally, then walks its own chunks.  A one-CTA cluster owns the whole
+// system: Y = Z = 0 and no exchange.
+//   ctl  this CTA's chunk maps (ct rows q0 .. q0+ncl-1, 12 values each)
+//   rsp  the cyclic rows' g per unit forward inflow (8 values)
+#ifdef FH_PROF
+#define FHP(i) do { if (pt) { long long _n = clock64(); pt[i] += _n - _t; _t = _n; } } while (0)
+#else
+#define FHP(i) do {} while (0)
+#endif
+template <typename T>
+__device__ __forceinline__ void ld4(const T *p, T *m)
 {
-    const int par = t & 1;
+    m[0] = p[0], m[1] = p[1], m[2] = p[2], m[3] = p[3];
+}
+__device__ __forceinline__ void st_peer2(uint32_t a, double x, double y)
+{
+    asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(x), "d"(y) : "memory");
+}
+__device__ __forceinline__ void st_peer2(uint32_t a, float x, float y)
+{
+    asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(x), "f"(y) : "memory");
+}
+__device__ __forceinline__ void st_peer(uint32_t a, double x)
+{
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(x) : "memory");
+}
+__device__ __forceinline__ void st_peer(uint32_t a, float x)
+{
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(x) : "memory");
+}
+template <typename T, int K, bool PER, int CSM, typename SM>
+__device__ void cluster_scan(const CArgs<T> &A, SM &S, const T *ctl, const T *rsp, int t, int c, int q0, int ncl,
+                             int lane, long long *pt = nullptr)
+{
+#ifdef FH_PROF
+    long long _t = clock64();
+#endif
+    const int par = SM::NPAR == 2 ? (t & 1) : 0;
     T(*R)[TW][4] = S.rec[par];
     // ---- forward fold, zero inflow: yin0_i, Phi_i; c0_i = zB_i + H_i yin0_i; Hc_i = H_i Phi_i
+    // (Phi, Hc, Pb, K: the responses to this CTA's inflows -- only a multi-CTA
+    // cluster needs them)
+    const bool multi = A.cs > 1;
+    int li[4];   // local chunk of each cyclic row (-1: not mine)
+#pragma unroll
+    for (int jx = 0; jx < 4; ++jx) {
+        const int64_t qq = A.srow[jx] >= 0 ? A.srow[jx] / Q - q0 : -1;
+        li[jx] = PER && qq >= 0 && qq < ncl ? (int)qq : -1;
+    }
     T Phi[4] = {T(1), T(0), T(0), T(1)}, y0 = T(0), y1 = T(0);
     T gj[4] = {T(0), T(0), T(0), T(0)}, rj[4][2] = {{T(0), T(0)}, {T(0), T(0)}, {T(0), T(0)}, {T(0), T(0)}};
     for (int i = 0; i < ncl; ++i) {
-        const int q = q0 + i;
-        T m[4], h[4], hc[4], t0, t1;
-        ldm4(A.ct + (int64_t)q * 12, m);
-        ldm4(A.ct + (int64_t)q * 12 + 8, h);
+        T m[4], h[4], t0, t1;
+        ld4(ctl + i * 12, m);
+        ld4(ctl + i * 12 + 8, h);
         const T yf0 = R[i][lane][0], yf1 = R[i][lane][1];
         mv(h, y0, y1, t0, t1);
         R[i][lane][0] = y0;            // yin0_i
         R[i][lane][1] = y1;
         R[i][lane][2] += t0;           // c0_i
         R[i][lane][3] += t1;
-        mmul(h, Phi, hc);
-        if (lane < 4) S.phi[i][lane] = Phi[lane], S.phi[i][4 + lane] = hc[lane];
         if (PER) {
 #pragma unroll
             for (int jx = 0; jx < 4; ++jx)
-                if (A.srow[jx] >= 0 && A.srow[jx] / Q == q) {
-                    gj[jx] = S.spec[par][jx][lane] + A.rsp[jx * 2] * y0 + A.rsp[jx * 2 + 1] * y1;
-                    rj[jx][0] = A.rsp[jx * 2] * Phi[0] + A.rsp[jx * 2 + 1] * Phi[2];
-                    rj[jx][1] = A.rsp[jx * 2] * Phi[1] + A.rsp[jx * 2 + 1] * Phi[3];
+                if (li[jx] == i) {
+                    gj[jx] = S.spec[par][jx][lane] + rsp[jx * 2] * y0 + rsp[jx * 2 + 1] * y1;
+                    rj[jx][0] = rsp[jx * 2] * Phi[0] + rsp[jx * 2 + 1] * Phi[2];
+                    rj[jx][1] = rsp[jx * 2] * Phi[1] + rsp[jx * 2 + 1] * Phi[3];
                 }
         }
         mv(m, y0, y1, t0, t1);
         y0 = t0 + yf0;
         y1 = t1 + yf1;
-        mmul(m, Phi, Phi);
+        if (multi) {
+            T hc[4];
+            mmul(h, Phi, hc);
+            if (lane < 4) S.phi[i][lane] = Phi[lane], S.phi[i][4 + lane] = hc[lane];
+            mmul(m, Phi, Phi);
+        }
     }
     __syncwarp();
+    FHP(0);
     // ---- backward fold, zero inflows: b = sum Mb.. c0_i, Pb = prod Mb, K = sum Mb.. Hc_i
     T Pb[4] = {T(1), T(0), T(0), T(1)}, Kc[4] = {T(0), T(0), T(0), T(0)}, b0 = T(0), b1 = T(0);
     for (int i = ncl - 1; i >= 0; --i) {
-        T m[4], t0, t1, hc[4];
-        ldm4(A.ct + (int64_t)(q0 + i) * 12 + 4, m);
+        T m[4], t0, t1;
+        ld4(ctl + i * 12 + 4, m);
         mv(m, b0, b1, t0, t1);
         b0 = t0 + R[i][lane][2];
         b1 = t1 + R[i][lane][3];
-        mmul(m, Pb, Pb);
-        mmul(m, Kc, Kc);
+        if (multi) {
+            mmul(m, Pb, Pb);
+            mmul(m, Kc, Kc);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            hc[e] = S.phi[i][4 + e];
-            Kc[e] += hc[e];
+            for (int e = 0; e < 4; ++e) Kc[e] += S.phi[i][4 + e];
         }
     }
-    // ---- the one exchange: my summary to every CTA of the cluster (once every
-    // CTA has consumed the previous group's)
-    if (t >= 1) wait_cluster(&S.xcons, (uint32_t)((t - 1) & 1));
-    for (int r = 0; r < A.cs; ++r) {
-        T *pa = peer(&S.xa[c][lane][0], r), *pb = peer(&S.xb[c][lane][0], r);
-        pa[0] = y0, pa[1] = y1;
-        pb[0] = b0, pb[1] = b1;
-        if (lane < 4) {
-            T *pp = peer(&S.xP[c][0], r);
-            pp[lane] = Phi[lane];
-            pp[4 + lane] = Pb[lane];
-            pp[8 + lane] = Kc[lane];
+    FHP(1);
+    T Zc0 = T(0), Zc1 = T(0), y1c = b0, y2c = b1;   // one CTA: Y = Z = 0, (x_0, x_1) = my outflow
+    T gv[4] = {gj[0], gj[1], gj[2], gj[3]};
+    if (multi) {
+        // ---- the one exchange: my summary to every CTA of the cluster (once every
+        // CTA has consumed the previous group's)
+        if (t >= 1) wait_cluster(&S.xcons, (uint32_t)((t - 1) & 1));
+        FHP(2);
+        for (int r = 0; r < A.cs; ++r) {
+            st_peer2(mapa(&S.xa[c][lane][0], r), y0, y1);
+            st_peer2(mapa(&S.xb[c][lane][0], r), b0, b1);
+            if (lane < 4) {
+                const uint32_t pp = mapa(&S.xP[c][0], r);
+                st_peer(pp + lane * sizeof(T), Phi[lane]);
+                st_peer(pp + (4 + lane) * sizeof(T), Pb[lane]);
+                st_peer(pp + (8 + lane) * sizeof(T), Kc[lane]);
+            }
+            if (PER) {
+#pragma unroll
+                for (int jx = 0; jx < 4; ++jx)
+                    if (A.srow[jx] >= 0 && A.srow[jx] / Q >= q0 && A.srow[jx] / Q < q0 + ncl) {
+                        st_peer(mapa(&S.xg[jx][lane], r), gj[jx]);
+                        if (lane < 2) st_peer(mapa(&S.xr[jx][lane], r), rj[jx][lane]);
+                    }
+            }
         }
+        fence_cluster();
+        __syncwarp();
+        if (lane == 0)
+            for (int r = 0; r < A.cs; ++r) arrive_remote(&S.xch, r);
+        FHP(3);
+        wait_cluster(&S.xch, (uint32_t)(t & 1));
+        FHP(4);
+        // ---- every CTA's forward inflow Y_v (kept per lane in S.yv), then backward inflows from the top
+        {
+            T ya = T(0), yb = T(0);
+            for (int v = 0; v < A.cs; ++v) {
+                S.yv[v][lane][0] = ya, S.yv[v][lane][1] = yb;
+                T t0, t1;
+                mv(S.xP[v], ya, yb, t0, t1);
+                ya = t0 + S.xa[v][lane][0];
+                yb = t1 + S.xa[v][lane][1];
+            }
+        }
+        T Za = T(0), Zb = T(0);   // running backward inflow
+        for (int v = A.cs - 1; v >= 0; --v) {
+            if (v == c) Zc0 = Za, Zc1 = Zb;
+            T t0, t1, u0, u1;
+            mv(S.xP[v] + 4, Za, Zb, t0, t1);
+            mv(S.xP[v] + 8, S.yv[v][lane][0], S.yv[v][lane][1], u0, u1);
+            Za = t0 + u0 + S.xb[v][lane][0];
+            Zb = t1 + u1 + S.xb[v][lane][1];
+        }
+        y1c = Za, y2c = Zb;
+        // cyclic rows' g (read now: the exchange buffer is released right after)
         if (PER) {
 #pragma unroll
             for (int jx = 0; jx < 4; ++jx)
-                if (A.srow[jx] >= 0 && A.srow[jx] / Q >= q0 && A.srow[jx] / Q < q0 + ncl) {
-                    peer(&S.xg[jx][0], r)[lane] = gj[jx];
-                    if (lane < 2) peer(&S.xr[jx][0], r)[lane] = rj[jx][lane];
+                if (A.srow[jx] >= 0) {
+                    const int ow = (int)(A.srow[jx] / Q) / A.cpc;   // owner CTA of the row's chunk
+                    gv[jx] = S.xg[jx][lane] + S.xr[jx][0] * S.yv[ow][lane][0] + S.xr[jx][1] * S.yv[ow][lane][1];
                 }
         }
-    }
-    fence_cluster();
-    __syncwarp();
-    if (lane == 0)
-        for (int r = 0; r < A.cs; ++r) arrive_remote(&S.xch, r);
-    wait_cluster(&S.xch, (uint32_t)(t & 1));
-    // ---- every CTA's forward inflow Y_v, then backward inflows from the top
-    T Yv[CSMAX][2];
-    {
-        T ya = T(0), yb = T(0);
-        for (int v = 0; v < A.cs; ++v) {
-            Yv[v][0] = ya, Yv[v][1] = yb;
-            T t0, t1;
-            mv(S.xP[v], ya, yb, t0, t1);
-            ya = t0 + S.xa[v][lane][0];
-            yb = t1 + S.xa[v][lane][1];
+        fence_cluster();
+        __syncwarp();
+        if (lane == 0)
+            for (int r = 0; r < A.cs; ++r) arrive_remote(&S.xcons, r);   // this group's exchange consumed
+        FHP(5);
+        // ---- my chunks: yin_i = yin0_i + Phi_i Y, c_i = c0_i + Hc_i Y
+        const T Y0 = S.yv[c][lane][0], Y1 = S.yv[c][lane][1];
+        for (int i = 0; i < ncl; ++i) {
+            T t0, t1, u0, u1;
+            mv(S.phi[i], Y0, Y1, t0, t1);
+            mv(S.phi[i] + 4, Y0, Y1, u0, u1);
+            R[i][lane][0] += t0;
+            R[i][lane][1] += t1;
+            R[i][lane][2] += u0;
+            R[i][lane][3] += u1;
         }
     }
-    T Za = T(0), Zb = T(0), Zc0 = T(0), Zc1 = T(0);   // running backward inflow; mine
-    for (int v = A.cs - 1; v >= 0; --v) {
-        if (v == c) Zc0 = Za, Zc1 = Zb;
-        T t0, t1, u0, u1;
-        mv(S.xP[v] + 4, Za, Zb, t0, t1);
-        mv(S.xP[v] + 8, Yv[v][0], Yv[v][1], u0, u1);
-        Za = t0 + u0 + S.xb[v][lane][0];
-        Zb = t1 + u1 + S.xb[v][lane][1];
-    }
-    // cyclic rows' g (read now: the exchange buffer is released right after)
-    T gv[4] = {T(0), T(0), T(0), T(0)};
-    if (PER) {
-#pragma unroll
-        for (int jx = 0; jx < 4; ++jx)
-            if (A.srow[jx] >= 0) {
-                const int ow = (int)(A.srow[jx] / Q) / A.cpc;   // owner CTA of the row's chunk
-                gv[jx] = S.xg[jx][lane] + S.xr[jx][0] * Yv[ow][0] + S.xr[jx][1] * Yv[ow][1];
-            }
-    }
-    fence_cluster();
-    __syncwarp();
-    if (lane == 0)
-        for (int r = 0; r < A.cs; ++r) arrive_remote(&S.xcons, r);   // this group's exchange consumed
-    // ---- my chunks: yin_i = yin0_i + Phi_i Y, c_i = c0_i + Hc_i Y; zin walk from Z_c
-    const T Y0 = Yv[c][0], Y1 = Yv[c][1];
-    for (int i = 0; i < ncl; ++i) {
-        T t0, t1, u0, u1;
-        mv(S.phi[i], Y0, Y1, t0, t1);
-        mv(S.phi[i] + 4, Y0, Y1, u0, u1);
-        R[i][lane][0] += t0;
-        R[i][lane][1] += t1;
-        R[i][lane][2] += u0;
-        R[i][lane][3] += u1;
-    }
+    // ---- zin walk from Z_c
     T z0 = Zc0, z1 = Zc1;
     for (int i = ncl - 1; i >= 0; --i) {
         T m[4], t0, t1;
-        ldm4(A.ct + (int64_t)(q0 + i) * 12 + 4, m);
+        ld4(ctl + i * 12 + 4, m);
         const T cq0 = R[i][lane][2], cq1 = R[i][lane][3];
         R[i][lane][2] = z0;
         R[i][lane][3] = z1;
@@ -261,9 +316,9 @@ __device__ void cluster_scan(const CArgs<T> &A, CSmem<T, MODE> &S, int t, int c,
         z0 = t0 + cq0;
         z1 = t1 + cq1;
     }
+    FHP(6);
     if (!PER) return;
     // ---- cyclic pair: (x_0, x_1) = CTA 0's backward outflow; g on the cyclic rows
-    const T y1c = Za, y2c = Zb;
     const double *sc = A.scal;
     T xl0, xl1;
     if (K == 2) {
@@ -280,6 +335,7 @@ __device__ void cluster_scan(const CArgs<T> &A, CSmem<T, MODE> &S, int t, int c,
     }
     S.xl[par][lane][0] = xl0;
     S.xl[par][lane][1] = xl1;
+    FHP(7);
 }
 
 // ---------------------------------------------------------------- item order of one CTA
@@ -308,8 +364,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fc_kernel(const __grid_constant__
 {
     using C = CCfg<T, MODE>;
     constexpr int NS = C::NS, TILE = C::TILE;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    CSmem<T, MODE> &sm = *reinterpret_cast<CSmem<T, MODE> *>((((uintptr_t)smem_raw) + 1023) & ~(uintptr_t)1023);
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1 KB aligned (the 128B swizzle of contiguous tiles); derived from smem_raw
+    // by pointer arithmetic so the compiler keeps the shared address space
+    CSmem<T, MODE> &sm = *reinterpret_cast<CSmem<T, MODE> *>(smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = (int)cg::this_cluster().block_rank();
     const int cl = blockIdx.x / A.cs;                       // cluster index
@@ -546,7 +604,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fc_kernel(const __grid_constant__
         for (int t = 0; t < T_; ++t) {
             const int par = t & 1;
             if (ncl > 0) bar_wait(&sm.p1done[par], (uint32_t)((t >> 1) & 1));
-            if (!(A.dbg & 1)) cluster_scan<T, K, PER, MODE>(A, sm, t, c, q0, ncl, lane);
+            if (!(A.dbg & 1)) cluster_scan<T, K, PER, CSMAX>(A, sm, A.ct + (int64_t)q0 * 12, A.rsp, t, c, q0, ncl, lane);
             __syncwarp();
             if (lane == 0) bar_arrive(&sm.scandone[par]);
         }

@@ -8,6 +8,7 @@
 
 #include "band_tile.cuh"
 #include "fused_cluster.cuh"
+#include "fused_hold.cuh"
 
 namespace pb {
 
@@ -162,6 +163,7 @@ static int fc_launch_t(const Band *h, T *x, T *xout, double alpha, int64_t count
     A.cs = best_cs;
     A.cpc = best_cpc;
     A.ncl = best_ncl;
+    A.prof = nullptr;
     {
         static const int dbg = getenv("PB_DEV_DBG") ? atoi(getenv("PB_DEV_DBG")) : 0;   // DEV ONLY
         static const int csf = getenv("PB_DEV_CS") ? atoi(getenv("PB_DEV_CS")) : 0;     // DEV ONLY
@@ -182,6 +184,131 @@ static int fc_launch_t(const Band *h, T *x, T *xout, double alpha, int64_t count
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = best_cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    PB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tmap, A));
+    PB_LAUNCH_CHECK();
+    return PB_OK;
+}
+
+// ---------------------------------------------------------------- held-tile kernel launcher
+// Cluster size CS = ceil(nq / NW) (one chunk per consumer warp), cpc =
+// ceil(nq / CS) chunks per CTA; clusters = the occupancy API's maximum (each
+// loops over groups).  PB_EUNSUPPORTED when nq > CSM * NW or the cluster does
+// not fit the GPU (the two-pass cluster kernel serves).
+template <typename T, int K, bool PER, int MODE, int LAY>
+static int fh_launch_t(const Band *h, T *x, T *xout, double alpha, int64_t count, int64_t bstride, cudaStream_t st,
+                       int64_t Mo, int64_t pitch, int *info = nullptr)
+{
+    constexpr int CSM = fh::csmax<MODE>();
+    auto kern = fh::fh_kernel<T, K, PER, MODE, LAY>;
+    const size_t smem = sizeof(fh::HSmem<T, MODE>) + 1024;
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    static int ncl_of[CSM + 1];
+    std::call_once(once, [&] {
+        attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (attr == cudaSuccess) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaGetLastError();
+        for (int cs = 1; cs <= CSM; ++cs) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)(cs * 16));
+            cfg.blockDim = dim3(fh::NTHREADS);
+            cfg.dynamicSmemBytes = smem;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = cs;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int ncl = 0;
+            if (attr == cudaSuccess && cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess) ncl = 0;
+            cudaGetLastError();
+            ncl_of[cs] = ncl;
+        }
+    });
+    if (attr != cudaSuccess) return PB_EUNSUPPORTED;
+    const int64_t M = Mo > 0 ? Mo : h->batch, n = h->n;
+    const int64_t P = pitch > 0 ? pitch : (LAY == fs::LAY_CONTIG ? n : M);
+    const int nq = h->fplan.nq;
+    const int64_t Gb = (M + fs::TW - 1) / fs::TW, G = Gb * count;
+    const int cs = (nq + fh::NW - 1) / fh::NW;
+    if (G > (1 << 30) || cs > CSM || ncl_of[cs] < 1) return PB_EUNSUPPORTED;
+    const int cpc = (nq + cs - 1) / cs;
+    const int ncl = (int)std::min<int64_t>(ncl_of[cs], G);
+    if (info) {
+        info[0] = cs;
+        info[1] = cpc;
+        info[2] = ncl;
+        info[3] = 2;
+        return PB_OK;
+    }
+    fc::CArgs<T> A;
+    CUtensorMap tmap;
+    {
+        std::lock_guard<std::mutex> lk(h->fplan.mu);
+        FusedScratch &S = h->fplan.scratch[st];
+        bool flat = false;
+        int rc = tensor_map_for<T, LAY>(S, x, M, n, count, bstride, P, &tmap, &flat);
+        if (rc) return rc;
+        A.flat = flat ? 1 : 0;
+    }
+    A.rec = (const T *)h->fplan.rec;
+    A.coef = (const T *)h->coef;
+    A.ct = (const T *)h->fplan.ct;
+    A.rsp = (const T *)h->fplan.rsp;
+    A.scal = h->scal;
+    A.x = x;
+    A.xout = xout;
+    A.alpha = (T)alpha;
+    A.n = n;
+    A.M = M;
+    A.bstride = count > 1 ? bstride : P * (LAY == fs::LAY_CONTIG ? M : n);
+    A.pitch = P;
+    for (int j = 0; j < 4; ++j) A.srow[j] = h->srow[j];
+    A.nq = nq;
+    A.count = (int)count;
+    A.Gb = (int)Gb;
+    A.G = (int)G;
+    A.cs = cs;
+    A.cpc = cpc;
+    A.ncl = ncl;
+    A.dbg = 0;
+    A.prof = nullptr;
+#ifdef FH_PROF
+    static long long *dprof = nullptr;
+    static long long hprof[8 * 16];
+    static int nlaunch = 0;
+    if (!dprof) {
+        cudaMalloc(&dprof, sizeof(hprof));
+        cudaMemset(dprof, 0, sizeof(hprof));
+        atexit([] {
+            cudaMemcpy(hprof, dprof, sizeof(hprof), cudaMemcpyDeviceToHost);
+            fprintf(stderr, "FH_PROF launches %d (cycles per launch, summed over CTAs; per warp)\n", nlaunch);
+            const char *nm[16] = {"wait_full", "vload_issue", "P1", "wait_p1done", "scan", "wait_scandone", "P2", "store",
+                                  "s_fwd", "s_bwd", "s_xcons", "s_xwrite", "s_xwait", "s_resolve", "s_walk", "s_cyc"};
+            for (int w = 0; w < 8; ++w) {
+                fprintf(stderr, "w%d", w);
+                for (int i = 0; i < 16; ++i)
+                    if (hprof[w * 16 + i]) fprintf(stderr, " %s=%.0f", nm[i], (double)hprof[w * 16 + i] / nlaunch);
+                fprintf(stderr, "\n");
+            }
+        });
+    }
+    A.prof = dprof;
+    ++nlaunch;
+#endif
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(ncl * cs));
+    cfg.blockDim = dim3(fh::NTHREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
@@ -343,6 +470,16 @@ static int fs_launch_dl(const Band *h, void *x, int64_t count, int64_t bstride, 
     T *X = (T *)x;
     using namespace fs;
     int rc;
+    static const int nohold = getenv("PB_DEV_NOHOLD") ? atoi(getenv("PB_DEV_NOHOLD")) : 0;   // DEV ONLY
+    if (!nohold) {
+        if (h->K == 2)
+            rc = h->periodic ? fh_launch_t<T, 2, true, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch)
+                             : fh_launch_t<T, 2, false, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch);
+        else
+            rc = h->periodic ? fh_launch_t<T, 1, true, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch)
+                             : fh_launch_t<T, 1, false, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch);
+        if (rc != PB_EUNSUPPORTED) return rc;
+    }
     if (h->K == 2)
         rc = h->periodic ? fc_launch_t<T, 2, true, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch)
                          : fc_launch_t<T, 2, false, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch);
@@ -366,21 +503,39 @@ int FS_NAME(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t
 // diagnostics: the cluster configuration a solve of M systems x count would use
 int FS_INFO_NAME(const Band *h, int64_t M, int64_t count, int *info)
 {
+    int rc;
     if (h->K == 2)
-        return h->periodic ? fc_launch_t<FS_T, 2, true, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0,
+        rc = h->periodic ? fh_launch_t<FS_T, 2, true, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0,
+                                                                              nullptr, M, 0, info)
+                         : fh_launch_t<FS_T, 2, false, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0,
+                                                                               nullptr, M, 0, info);
+    else
+        rc = h->periodic ? fh_launch_t<FS_T, 1, true, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0,
+                                                                              nullptr, M, 0, info)
+                         : fh_launch_t<FS_T, 1, false, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0,
+                                                                               nullptr, M, 0, info);
+    if (rc != PB_EUNSUPPORTED) return rc;
+    info[3] = 1;
+    if (h->K == 2)
+        rc = h->periodic ? fc_launch_t<FS_T, 2, true, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0,
                                                                                  nullptr, M, 0, info)
                            : fc_launch_t<FS_T, 2, false, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0,
                                                                                   nullptr, M, 0, info);
-    return h->periodic ? fc_launch_t<FS_T, 1, true, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0, nullptr,
-                                                                             M, 0, info)
-                       : fc_launch_t<FS_T, 1, false, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0, nullptr,
-                                                                              M, 0, info);
+    else
+        rc = h->periodic ? fc_launch_t<FS_T, 1, true, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0,
+                                                                              nullptr, M, 0, info)
+                         : fc_launch_t<FS_T, 1, false, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0,
+                                                                               nullptr, M, 0, info);
+    if (info[0] == 0) info[3] = 0;
+    return rc;
 }
 
 #ifdef FS_CH1D_NAME
 int FS_CH1D_NAME(const Band *h, const void *c, void *cnew, double alpha, int64_t M, cudaStream_t st)
 {
-    int rc = fc_launch_t<FS_T, 2, true, fs::MODE_CH1D, fs::LAY_INTER>(h, (FS_T *)c, (FS_T *)cnew, alpha, 1, 0, st, M, 0);
+    int rc = fh_launch_t<FS_T, 2, true, fs::MODE_CH1D, fs::LAY_INTER>(h, (FS_T *)c, (FS_T *)cnew, alpha, 1, 0, st, M, 0);
+    if (rc != PB_EUNSUPPORTED) return rc;
+    rc = fc_launch_t<FS_T, 2, true, fs::MODE_CH1D, fs::LAY_INTER>(h, (FS_T *)c, (FS_T *)cnew, alpha, 1, 0, st, M, 0);
     if (rc != PB_EUNSUPPORTED) return rc;
     return fs_launch_t<FS_T, 2, true, fs::MODE_CH1D, fs::LAY_INTER>(h, (FS_T *)c, (FS_T *)cnew, alpha, 1, 0, st, M, 0);
 }

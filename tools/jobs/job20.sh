@@ -1,0 +1,2 @@
+python -c "import torch; torch.zeros(1).cuda()"
+for s in 512:262144 8192:8192 2048:2048; do timeout 100 python tools/fs_time.py f64 $s 2>&1 | tail -12; done
