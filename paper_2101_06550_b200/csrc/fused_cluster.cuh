@@ -45,8 +45,9 @@ struct CCfg {
     static constexpr int E1K = 1024 / (int)sizeof(T);
     static constexpr int SLOT = (TILE + COEF + HALO + E1K - 1) / E1K * E1K;   // 1 KB multiple (swizzle)
     static constexpr int NS = sizeof(T) == 8 ? 8 : 16;
-    // max chunks per CTA per group (records in shared memory)
-    static constexpr int CPC = MODE == MODE_CH1D ? 8 : (sizeof(T) == 8 ? 16 : 32);
+    // max chunks per CTA per group (records in shared memory; fp64: 15 keeps the
+    // plan inside the 227 KB opt-in limit with its 1 KB alignment slack)
+    static constexpr int CPC = MODE == MODE_CH1D ? 8 : (sizeof(T) == 8 ? 15 : 32);
     static_assert(NS % NWC == 0, "ring slots must be a multiple of the consumer warps");
 };
 

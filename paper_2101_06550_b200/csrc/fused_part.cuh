@@ -9,6 +9,7 @@
 #include "band_tile.cuh"
 #include "fused_cluster.cuh"
 #include "fused_hold.cuh"
+#include "twopass.cuh"
 
 namespace pb {
 
@@ -102,7 +103,7 @@ static int fc_launch_t(const Band *h, T *x, T *xout, double alpha, int64_t count
             ncl_of[cs] = ncl;
         }
     });
-    if (attr != cudaSuccess) return set_error(PB_ECUDA, "fc_kernel smem attribute: %s", cudaGetErrorString(attr));
+    if (attr != cudaSuccess) return PB_EUNSUPPORTED;   // the shared-memory plan does not fit: the global kernel serves
     const int64_t M = Mo > 0 ? Mo : h->batch, n = h->n;
     const int64_t P = pitch > 0 ? pitch : (LAY == fs::LAY_CONTIG ? n : M);
     const int nq = h->fplan.nq;
@@ -164,18 +165,7 @@ static int fc_launch_t(const Band *h, T *x, T *xout, double alpha, int64_t count
     A.cpc = best_cpc;
     A.ncl = best_ncl;
     A.prof = nullptr;
-    {
-        static const int dbg = getenv("PB_DEV_DBG") ? atoi(getenv("PB_DEV_DBG")) : 0;   // DEV ONLY
-        static const int csf = getenv("PB_DEV_CS") ? atoi(getenv("PB_DEV_CS")) : 0;     // DEV ONLY
-        A.dbg = dbg;
-        if (csf >= 1 && (nq + csf - 1) / csf <= C::CPC && ncl_of[csf] > 0) {
-            A.cs = csf;
-            A.cpc = (nq + csf - 1) / csf;
-            A.ncl = (int)std::min<int64_t>(ncl_of[csf], G);
-            best_cs = A.cs;
-            best_ncl = A.ncl;
-        }
-    }
+    A.dbg = 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(best_ncl * best_cs));
     cfg.blockDim = dim3(fc::NTHREADS);
@@ -315,6 +305,146 @@ static int fh_launch_t(const Band *h, T *x, T *xout, double alpha, int64_t count
     cfg.numAttrs = 1;
     PB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tmap, A));
     PB_LAUNCH_CHECK();
+    return PB_OK;
+}
+
+
+// ---------------------------------------------------------------- two-pass launcher (interleaved)
+// P1 (+ group scans) then P2 as its programmatic dependent.  Consumer warps
+// per CTA and ring depth per warp: fp64 4 x 2 (P1 152 KB, P2 172 KB of
+// slots), fp32 4 x 4.
+#ifndef TP_NC1_64
+#define TP_NC1_64 4
+#define TP_R1_64 2
+#define TP_NC2_64 4
+#define TP_R2_64 2
+#define TP_NC1_32 4
+#define TP_R1_32 4
+#define TP_NC2_32 4
+#define TP_R2_32 4
+#endif
+template <typename T>
+struct TpCfg {
+    static constexpr int NC1 = sizeof(T) == 8 ? TP_NC1_64 : TP_NC1_32, R1 = sizeof(T) == 8 ? TP_R1_64 : TP_R1_32;
+    static constexpr int NC2 = sizeof(T) == 8 ? TP_NC2_64 : TP_NC2_32, R2 = sizeof(T) == 8 ? TP_R2_64 : TP_R2_32;
+};
+
+template <typename T, int K, bool PER>
+static int tp_launch_t(const Band *h, T *x, int64_t count, int64_t bstride, cudaStream_t st, int64_t Mo, int64_t pitch)
+{
+    constexpr int NC = TpCfg<T>::NC1, R = TpCfg<T>::R1, NC2 = TpCfg<T>::NC2, R2 = TpCfg<T>::R2;
+    auto k1 = tp::tp_p1_kernel<T, K, PER, NC, R>;
+    auto k2 = tp::tp_p2_kernel<T, K, PER, NC2, R2>;
+    auto ks = tp::tp_scan_kernel<T, K, PER>;
+    const size_t sm1 = sizeof(tp::P1Smem<T, NC, R>) + 1024;
+    const size_t sm2 = sizeof(tp::P2Smem<T, NC2, R2>) + 1024;
+    const size_t sms = (sizeof(tp::ScanSmem<T>) + 15) / 16 * 16 + sizeof(T) * 12 * (size_t)h->fplan.nq;
+    if (h->fplan.nq > tp::SL * tp::SEGMAX) return PB_EUNSUPPORTED;   // longer systems: the global kernel serves
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    std::call_once(once, [&] {
+        attr = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+        if (attr == cudaSuccess) attr = cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (attr == cudaSuccess) attr = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+        cudaGetLastError();
+    });
+    if (attr != cudaSuccess) return set_error(PB_ECUDA, "tp kernels smem attribute: %s", cudaGetErrorString(attr));
+    const int64_t M = Mo > 0 ? Mo : h->batch, n = h->n;
+    const int64_t P = pitch > 0 ? pitch : M;
+    const int nq = h->fplan.nq;
+    const int64_t Gb = (M + fs::TW - 1) / fs::TW, G = Gb * count;
+    if (G > (1 << 30)) return PB_EUNSUPPORTED;
+    const int64_t ntiles = G * nq;
+    if (ntiles >= ((int64_t)1 << 31)) return PB_EUNSUPPORTED;
+    const size_t es = sizeof(T);
+    tp::Args<T> A;
+    CUtensorMap tmap;
+    std::lock_guard<std::mutex> lk(h->fplan.mu);
+    FusedScratch &S = h->fplan.scratch[st];
+    // [cnt: tcnt counters, zeroed at allocation][car][spec][xl]
+    const size_t off_car = ((size_t)std::max<int64_t>(G, S.tcnt) * 4 + 255) / 256 * 256;
+    const size_t off_spec = off_car + es * (size_t)ntiles * 4 * fs::TW, off_xl = off_spec + es * (size_t)G * 4 * fs::TW;
+    const size_t need = off_xl + es * (size_t)G * 2 * fs::TW;
+    if (need > S.tbytes || G > S.tcnt) {
+        if (S.tbuf) {
+            PB_CUDA_TRY(cudaStreamSynchronize(st));   // queued solves may still use the old scratch
+            cudaFree(S.tbuf);
+            S.tbuf = nullptr;
+            S.tbytes = 0;
+        }
+        PB_CUDA_TRY(cudaMalloc(&S.tbuf, need));
+        PB_CUDA_TRY(cudaMemsetAsync(S.tbuf, 0, off_car, st));
+        S.tbytes = need;
+        S.tcnt = (int64_t)(off_car / 4);
+    }
+    {
+        bool flat = false;
+        int rc = tensor_map_for<T, fs::LAY_INTER>(S, x, M, n, count, bstride, P, &tmap, &flat);
+        if (rc) return rc;
+        A.flat = flat ? 1 : 0;
+    }
+    char *base = (char *)S.tbuf;
+    A.rec = (const T *)h->fplan.rec;
+    A.coef = (const T *)h->coef;
+    A.ct = (const T *)h->fplan.ct;
+    A.rsp = (const T *)h->fplan.rsp;
+    A.scal = h->scal;
+    A.x = x;
+    A.cnt = (unsigned *)base;
+    A.car = (T *)(base + off_car);
+    A.spec = (T *)(base + off_spec);
+    A.xl = (T *)(base + off_xl);
+    A.n = n;
+    A.M = M;
+    A.bstride = count > 1 ? bstride : P * n;
+    A.pitch = P;
+    A.ntiles = ntiles;
+    // the last ~48 MB of f that P1 reads stay in L2 for P2's first (reversed) tiles
+    const int64_t keep = (int64_t)(48.0 * 1048576.0 / (double)(fs::Q * fs::TW * es));
+    A.keep_from = ntiles > keep ? ntiles - keep : 0;
+    for (int j = 0; j < 4; ++j) A.srow[j] = h->srow[j];
+    A.nq = nq;
+    A.Gb = (int)Gb;
+    A.G = (int)G;
+    A.BG = (int)G;   // one band: chunk-major order over all groups (contiguous row blocks)
+    const unsigned grid = (unsigned)std::min<int64_t>(fs_sm_count(), (ntiles + NC - 1) / NC);
+    const unsigned grid2 = (unsigned)std::min<int64_t>(fs_sm_count(), (ntiles + NC2 - 1) / NC2);
+    k1<<<grid, 32 * NC, sm1, st>>>(tmap, A);
+    PB_LAUNCH_CHECK();
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)G);
+        cfg.blockDim = dim3(32 * ((nq + tp::SL - 1) / tp::SL));
+        cfg.dynamicSmemBytes = sms;
+        cfg.stream = st;
+        cfg.attrs = pdl;
+        cfg.numAttrs = 1;
+        PB_CUDA_TRY(cudaLaunchKernelEx(&cfg, ks, A));
+        PB_LAUNCH_CHECK();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid2);
+    cfg.blockDim = dim3(32 * NC2);
+    cfg.dynamicSmemBytes = sm2;
+    cfg.stream = st;
+    cfg.attrs = pdl;
+    cfg.numAttrs = 1;
+    PB_CUDA_TRY(cudaLaunchKernelEx(&cfg, k2, tmap, A));
+    PB_LAUNCH_CHECK();
+#ifdef TP_PROF
+    static int nl = 0;
+    if (nl++ == 0)
+        atexit([] {
+            unsigned long long hp[16];
+            cudaMemcpyFromSymbol(hp, tp::tp_prof, sizeof(hp));
+            fprintf(stderr, "TP_PROF (cycles summed over warps, all launches):");
+            for (int i = 0; i < 16; ++i) fprintf(stderr, " %d=%.3g", i, (double)hp[i]);
+            fprintf(stderr, "\n");
+        });
+#endif
     return PB_OK;
 }
 
@@ -470,8 +600,19 @@ static int fs_launch_dl(const Band *h, void *x, int64_t count, int64_t bstride, 
     T *X = (T *)x;
     using namespace fs;
     int rc;
-    static const int nohold = getenv("PB_DEV_NOHOLD") ? atoi(getenv("PB_DEV_NOHOLD")) : 0;   // DEV ONLY
-    if (!nohold) {
+    // interleaved systems longer than one held-tile CTA (8 chunks): the
+    // two-pass kernels (P1 / scan / P2; measured 2.5x faster than the cluster
+    // exchange of the held-tile kernel at N = M = 8192)
+    if (LAY == LAY_INTER && h->fplan.nq > fh::NW) {
+        if (h->K == 2)
+            rc = h->periodic ? tp_launch_t<T, 2, true>(h, X, count, bstride, st, M, pitch)
+                             : tp_launch_t<T, 2, false>(h, X, count, bstride, st, M, pitch);
+        else
+            rc = h->periodic ? tp_launch_t<T, 1, true>(h, X, count, bstride, st, M, pitch)
+                             : tp_launch_t<T, 1, false>(h, X, count, bstride, st, M, pitch);
+        if (rc != PB_EUNSUPPORTED) return rc;
+    }
+    {
         if (h->K == 2)
             rc = h->periodic ? fh_launch_t<T, 2, true, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch)
                              : fh_launch_t<T, 2, false, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch);
@@ -480,6 +621,7 @@ static int fs_launch_dl(const Band *h, void *x, int64_t count, int64_t bstride, 
                              : fh_launch_t<T, 1, false, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch);
         if (rc != PB_EUNSUPPORTED) return rc;
     }
+    {
     if (h->K == 2)
         rc = h->periodic ? fc_launch_t<T, 2, true, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch)
                          : fc_launch_t<T, 2, false, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch);
@@ -487,6 +629,7 @@ static int fs_launch_dl(const Band *h, void *x, int64_t count, int64_t bstride, 
         rc = h->periodic ? fc_launch_t<T, 1, true, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch)
                          : fc_launch_t<T, 1, false, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch);
     if (rc != PB_EUNSUPPORTED) return rc;
+    }
     // beyond the cluster's shared-memory span: the global-scan kernel
     if (h->K == 2)
         return h->periodic ? fs_launch_t<T, 2, true, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch)
