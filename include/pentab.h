@@ -153,11 +153,13 @@ PB_API int pent_solve_strided(pb_penta_t h, void *rhs, const pb_layout *L, void 
 
 /* pent_solve_info — diagnostic: the configuration of the fused streaming
  * solve for one batch of the handle in `layout`; info points to 4 ints:
- * info[0] = thread-block cluster size CS (0 = N beyond the cluster span,
- * the global-scan kernel serves), info[1] = 64-row chunks per CTA,
- * info[2] = clusters launched, info[3] = kernel: 2 = tiles held on chip
- * between the two sweeps (f read once, N <= 16*8*64), 1 = two-pass cluster
- * kernel (f re-read through L2), 0 = global-scan kernel;
+ * info[0] = thread-block cluster size CS (0 = no clusters), info[1] =
+ * 64-row chunks per CTA, info[2] = clusters (CTAs) launched, info[3] =
+ * kernel: 3 = two-pass streaming kernels (interleaved, 8 < N/64 <= 128:
+ * P1 / segmented scan / P2, f re-read partly from L2), 2 = tiles held on
+ * chip between the two sweeps (f read once; interleaved N <= 512,
+ * contiguous N <= 16*8*64), 1 = two-pass cluster kernel, 0 = global-scan
+ * kernel (N beyond the cluster span);
  * all -1 when the handle has no fused plan: per-system LHS, or chunk maps
  * of the factored LHS that grow (max-abs entry >= 1 over a 64-row chunk,
  * e.g. kappa ~ 1e6+) -- such handles are solved one thread per system, the

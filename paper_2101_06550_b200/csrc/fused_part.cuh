@@ -647,6 +647,16 @@ int FS_NAME(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t
 int FS_INFO_NAME(const Band *h, int64_t M, int64_t count, int *info)
 {
     int rc;
+    if (FS_LAY == fs::LAY_INTER && h->fplan.nq > fh::NW && h->fplan.nq <= tp::SL * tp::SEGMAX &&
+        (int64_t)h->fplan.nq * ((M + fs::TW - 1) / fs::TW) * count < ((int64_t)1 << 31)) {
+        // the two-pass kernels: no clusters; info[2] = CTAs of P1
+        const int64_t nt = (int64_t)h->fplan.nq * ((M + fs::TW - 1) / fs::TW) * count;
+        info[0] = 0;
+        info[1] = 0;
+        info[2] = (int)std::min<int64_t>(fs_sm_count(), (nt + TpCfg<FS_T>::NC1 - 1) / TpCfg<FS_T>::NC1);
+        info[3] = 3;
+        return PB_OK;
+    }
     if (h->K == 2)
         rc = h->periodic ? fh_launch_t<FS_T, 2, true, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0,
                                                                               nullptr, M, 0, info)

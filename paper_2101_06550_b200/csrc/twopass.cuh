@@ -185,10 +185,11 @@ __device__ __forceinline__ unsigned char *smem_base()
 
 template <typename T>
 __device__ __forceinline__ void issue_tile(const CUtensorMap *tm, const Args<T> &A, int64_t g, int q, T *dst,
-                                           uint64_t *bar, const T *rows, uint32_t row_bytes, uint64_t pol)
+                                           uint64_t *bar, const T *rows, uint32_t row_bytes, uint64_t pol,
+                                           uint32_t extra_tx = 0)
 {
     const int b = (int)(g / A.Gb), gl = (int)(g - (int64_t)b * A.Gb);
-    bar_expect_tx(bar, (uint32_t)(Q * TW * sizeof(T)) + row_bytes);
+    bar_expect_tx(bar, (uint32_t)(Q * TW * sizeof(T)) + row_bytes + extra_tx);
     if (A.flat) tma_load2(dst, tm, gl * TW, (int)((int64_t)b * A.n + (int64_t)q * Q), bar, pol);
     else tma_load3(dst, tm, gl * TW, q * Q, b, bar, pol);
     bulk_load(dst + Q * TW, rows, row_bytes, bar);
@@ -501,7 +502,9 @@ __global__ void __launch_bounds__(32 * SEGMAX, 1) tp_scan_kernel(const Args<T> A
 // ---------------------------------------------------------------- P2
 template <typename T, int NC, int R>
 struct P2Smem {
-    static constexpr int SLOT = ((Q * TW + Q * COEF_STRIDE) * (int)sizeof(T) + 127) / 128 * 128 / (int)sizeof(T);
+    // tile | coefficient rows | the tile's inflows [4][TW] | x_l [2][TW]
+    static constexpr int INF = Q * TW + Q * COEF_STRIDE, XL = INF + 4 * TW;
+    static constexpr int SLOT = ((XL + 2 * TW) * (int)sizeof(T) + 127) / 128 * 128 / (int)sizeof(T);
     T slot[NC][R][SLOT];
     T cpriv[NC][Q * COEF_STRIDE];   // the current tile's coefficient rows (its slot is refilled early)
     uint64_t full[NC][R];
@@ -521,17 +524,30 @@ __global__ void __launch_bounds__(32 * NC, 1) tp_p2_kernel(const __grid_constant
     const uint64_t pol = fs::policy_evict_first();
     const uint32_t rb = (uint32_t)(Q * COEF_STRIDE * sizeof(T));
     auto tile_of = [&](int64_t i) { return A.ntiles - 1 - i; };   // reverse order: L2-warm tiles first
-    auto issue = [&](int64_t i, int r) {
+    // the tile's inflows and x_l ride in the slot (bulk copies on the same
+    // mbarrier: the tile's expect_tx covers them)
+    const uint32_t ib = (uint32_t)(4 * TW * sizeof(T)), xb = PER ? (uint32_t)(2 * TW * sizeof(T)) : 0u;
+    auto issue_in = [&](int64_t i, int r) {
         const TC tc = tile_coords(A, tile_of(i));
-        issue_tile<T>(&tmap, A, tc.g, tc.q, sm.slot[w][r], &sm.full[w][r], A.coef + (int64_t)tc.q * Q * COEF_STRIDE, rb,
-                      pol);
+        T *dst = sm.slot[w][r];
+        bulk_load(dst + S::INF, A.car + (tc.g * A.nq + tc.q) * 4 * TW, ib, &sm.full[w][r]);
+        if (PER) bulk_load(dst + S::XL, A.xl + tc.g * 2 * TW, xb, &sm.full[w][r]);
     };
-    // f and the coefficients are not written by P1: the first loads go out
-    // before the dependency wait
+    auto issue = [&](int64_t i, int r, bool with_in) {
+        const TC tc = tile_coords(A, tile_of(i));
+        issue_tile<T>(&tmap, A, tc.g, tc.q, sm.slot[w][r], &sm.full[w][r], A.coef + (int64_t)tc.q * Q * COEF_STRIDE,
+                      rb, pol, ib + xb);
+        if (with_in) issue_in(i, r);
+    };
+    // f and the coefficients are not written by P1 or the scan: the first
+    // tiles go out before the dependency wait, their inflows after it
     if (lane == 0)
         for (int r = 0; r < R; ++r)
-            if (W + r * NWT < A.ntiles) issue(W + r * NWT, r);
+            if (W + r * NWT < A.ntiles) issue(W + r * NWT, r, false);
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (lane == 0)
+        for (int r = 0; r < R; ++r)
+            if (W + r * NWT < A.ntiles) issue_in(W + r * NWT, r);
     T *cp = sm.cpriv[w];
     int k = 0;
     TPQ_INIT;
@@ -543,14 +559,13 @@ __global__ void __launch_bounds__(32 * NC, 1) tp_p2_kernel(const __grid_constant
         const int64_t r0 = (int64_t)q * Q;
         const int kmax = (int)min((int64_t)Q, A.n - r0);
         const int b = (int)(g / A.Gb), gl = (int)(g - (int64_t)b * A.Gb);
-        // the tile's inflows (L2; their latency overlaps the tile's arrival)
-        const T *pin = A.car + (g * A.nq + q) * 4 * TW + lane;
-        const T yi0 = __ldcg(pin), yi1 = __ldcg(pin + TW), zi0 = __ldcg(pin + 2 * TW), zi1 = __ldcg(pin + 3 * TW);
-        T xl0 = T(0), xl1 = T(0);
-        if (PER) xl0 = __ldcg(A.xl + (g * 2) * TW + lane), xl1 = __ldcg(A.xl + (g * 2 + 1) * TW + lane);
         bar_wait(&sm.full[w][r], (uint32_t)((k / R) & 1));
         TPQ(8);
         const T *d = sm.slot[w][r];
+        const T yi0 = d[S::INF + lane], yi1 = d[S::INF + TW + lane], zi0 = d[S::INF + 2 * TW + lane],
+                zi1 = d[S::INF + 3 * TW + lane];
+        T xl0 = T(0), xl1 = T(0);
+        if (PER) xl0 = d[S::XL + lane], xl1 = d[S::XL + TW + lane];
         T v[Q];
 #pragma unroll
         for (int kk = 0; kk < Q; ++kk) v[kk] = d[kk * TW + lane];
@@ -594,7 +609,7 @@ __global__ void __launch_bounds__(32 * NC, 1) tp_p2_kernel(const __grid_constant
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             if (i + R * NWT < A.ntiles) {
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                issue(i + R * NWT, r);
+                issue(i + R * NWT, r, true);
             }
         }
         __syncwarp();
@@ -603,14 +618,14 @@ __global__ void __launch_bounds__(32 * NC, 1) tp_p2_kernel(const __grid_constant
             TPQ(9);
             p2_fwd<T, K>(v, cp, yi0, yi1);
             __syncwarp();   // the slot's values are consumed: refill it
-            if (lane == 0 && i + R * NWT < A.ntiles) issue(i + R * NWT, r);
+            if (lane == 0 && i + R * NWT < A.ntiles) issue(i + R * NWT, r, true);
             TPQ(10);
             p2_bwd<T, K, PER>(v, cp, zi0, zi1, xl0, xl1);
             TPQ(11);
         } else {
             fs::tile_solve<T, K, PER, false>(v, cp, kmax, yi0, yi1, zi0, zi1, xl0, xl1);
             __syncwarp();
-            if (lane == 0 && i + R * NWT < A.ntiles) issue(i + R * NWT, r);
+            if (lane == 0 && i + R * NWT < A.ntiles) issue(i + R * NWT, r, true);
         }
         if (PER && K == 2 && r0 + Q > A.n - 2) {
             const int k2 = (int)(A.n - 2 - r0);

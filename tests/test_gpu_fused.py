@@ -226,10 +226,11 @@ def test_host_buffer_pipelined(pinned):
 @pytest.mark.parametrize("n,sigma", [(3000, 45.09), (700, 68.0), (2000, 2700.0), (130, 2700.0), (8192, 45.09),
                                      (12000, 45.09), (20000, 45.09)])
 def test_cluster_and_global_paths(n, sigma, dtype):
-    """The fused solve's three kernels against the oracle: the held-tile
-    kernel for N <= 16 x 8 chunks of 64 rows (n <= 8192), the two-pass cluster
-    kernel beyond it within its span (128 chunks fp64, 256 fp32: n = 12000
-    fp32), the global-scan kernel beyond that (n = 12000 fp64, n = 20000).
+    """The interleaved solve's kernels against the oracle: the held-tile kernel
+    for N <= 8 chunks of 64 rows (n = 130), the two-pass streaming kernels for
+    8 < N/64 <= 128 (n = 700 .. 8192), the two-pass cluster kernel beyond
+    within its span (256 chunks fp32: n = 12000 fp32), the global-scan kernel
+    beyond that (n = 12000 fp64, n = 20000).
     Cyclic (Navon), the thesis operators (sigma 45-68) and a slowly decaying
     one (sigma 2700: kappa 4.3e4), ragged n."""
     m = 200
@@ -239,9 +240,11 @@ def test_cluster_and_global_paths(n, sigma, dtype):
     h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in diags], batch=m, n=n, periodic=True, dtype=dtype)
     cs, cpc, ncl, kind = h.solve_info()
     nq = (n + 63) // 64
-    if nq <= 16 * 8:        # held tiles: one chunk per consumer warp (8), clusters up to 16
-        assert kind == 2 and cs == (nq + 7) // 8 and cpc <= 8 and cs * cpc >= nq and ncl >= 1, (cs, cpc, ncl, kind)
-    elif nq > (128 if dtype == "f64" else 256):   # CSMAX 8 x chunks per CTA (16 fp64, 32 fp32)
+    if nq <= 8:             # held tiles: one chunk per consumer warp (8), one CTA per group
+        assert kind == 2 and cs == 1 and cpc == nq and ncl >= 1, (cs, cpc, ncl, kind)
+    elif nq <= 128:         # two-pass streaming kernels
+        assert kind == 3 and cs == 0 and ncl >= 1, (cs, cpc, ncl, kind)
+    elif nq > (120 if dtype == "f64" else 256):   # CSMAX 8 x chunks per CTA (15 fp64, 32 fp32)
         assert cs == 0 and kind == 0
     else:
         assert kind == 1 and cs >= 1 and cs * cpc >= nq and ncl >= 1, (cs, cpc, ncl, kind)

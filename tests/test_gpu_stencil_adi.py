@@ -141,3 +141,33 @@ def test_table_3_1_on_gpu():
         e = oracle.convergence_error_2d(runs[n], runs[n // 2], 2 * math.pi)
         print(f"E_{n} = {e:.6f} (paper {rows[n]})")
         assert abs(e - rows[n]) <= 5e-5
+
+
+@pytest.mark.timeout(900)
+def test_adi_cfg4_shape_sampled_sims():
+    """configs[3] launch shape (512 sims x 512^2, L = 4 pi, the bench's sharding
+    unit) for 2 steps; sims 0, 1, 255, 511 against the oracle (each simulation
+    is independent, so a sampled sim is an exact check of the full launch)."""
+    sims, n = 512, 512
+    L = n * synth.DX_STATS
+    dt = synth.ch_dt(n, L)
+    c0 = synth.ch_ic_random(sims, n, seed=4)
+    gn, gm = gpu_adi(c0, 2, dt=dt, L=L)
+    for k in (0, 1, 255, 511):
+        rn, rm = oracle.ch_adi_steps(c0[k:k + 1], c0[k:k + 1], 2, dt=dt, D=1.0, gamma=0.01, L=L)
+        assert relerr(gn[k:k + 1], rn) <= 1e-12, k
+        assert relerr(gm[k:k + 1], rm) <= 1e-12, k
+
+
+@pytest.mark.timeout(1200)
+def test_adi_16384_single_grid():
+    """configs[4] grid size on one GPU: one 16384^2 simulation (L = 128 pi), one
+    ADI step through ch_adi_step against the oracle's full step (fp64)."""
+    n = 16384
+    L = n * synth.DX_STATS
+    dt = synth.ch_dt(n, L)
+    c0 = synth.ch_ic_random(1, n, seed=5)
+    rn, _ = oracle.ch_adi_steps(c0, c0, 1, dt=dt, D=1.0, gamma=0.01, L=L)
+    gn, gm = gpu_adi(c0, 1, dt=dt, L=L)
+    assert relerr(gn, rn) <= 1e-12
+    assert np.array_equal(gm, c0)
