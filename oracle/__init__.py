@@ -65,6 +65,13 @@ def lib():
         L.orc_ch_rhs.argtypes = [I64, I64, D, D, D, D, P, P, P]
         L.orc_ch_adi_steps.argtypes = [I64, I64, D, D, D, D, I64, P, P]
         L.orc_ch1d_steps.argtypes = [I64, I64, D, D, D, I64, P]
+        U64 = ctypes.c_uint64
+        L.orc_ch_free_energy.argtypes = [I64, I64, D, D, P, P]
+        L.orc_coarsening_beta.argtypes = [I64, I64, P, P, P]
+        L.orc_cook_rho.argtypes = [U64, I64, I64, I64, P, P]
+        L.orc_cook_rho.restype = None
+        L.orc_cook_noise.argtypes = [I64, I64, D, D, D, U64, I64, P]
+        L.orc_ch_adi_steps_cook.argtypes = [I64, I64, D, D, D, D, D, U64, I64, I64, P, P]
         _lib = L
     return _lib
 
@@ -193,6 +200,50 @@ def ch1d_steps(c, nsteps, *, n, m, dt, gamma, L):
     rc = lib().orc_ch1d_steps(n, m, dt, gamma, L, nsteps, _p(c))
     _check(rc)
     return c
+
+
+# ----------------------------------------------------------------- coarsening statistics
+def ch_free_energy(c, *, L, gamma):
+    """F of P:819-825 per simulation (reading r24: periodic forward differences)."""
+    c = _f64(c)
+    n = c.shape[-1]
+    sims = c.size // (n * n)
+    F = np.zeros(sims)
+    _check(lib().orc_ch_free_energy(sims, n, L, gamma, _p(c), _p(F)))
+    return F
+
+
+def coarsening_beta(t, F):
+    """beta = -(t/F) dF/dt from samples F[k][sim] at times t[k] (reading r27)."""
+    t, F = _f64(t), _f64(F)
+    nt = t.shape[0]
+    F2 = F.reshape(nt, -1)
+    beta = np.zeros_like(F2)
+    _check(lib().orc_coarsening_beta(nt, F2.shape[1], _p(t), _p(F2), _p(beta)))
+    return beta.reshape(F.shape)
+
+
+def cook_rho(seed, step, sim, cell):
+    """The counter-based N(0,1) pair (rho_x, rho_y) of one cell (reading r26)."""
+    rx, ry = np.zeros(1), np.zeros(1)
+    lib().orc_cook_rho(seed, step, sim, cell, _p(rx), _p(ry))
+    return float(rx[0]), float(ry[0])
+
+
+def cook_noise(sims, n, *, dt, L, sigma, seed, step):
+    """eta = sqrt(sigma/(dx^2 dt)) div rho, central differences (r26)."""
+    eta = np.zeros((sims, n, n))
+    _check(lib().orc_cook_noise(sims, n, dt, L, sigma, seed, step, _p(eta)))
+    return eta
+
+
+def ch_adi_steps_cook(cn, cm, nsteps, *, dt, D, gamma, L, sigma, seed, step0=0):
+    """Eq 3.1 with the Cahn–Hilliard–Cook noise + 2/3 dt eta^n in the RHS (r25)."""
+    cn, cm = _f64(cn).copy(), _f64(cm).copy()
+    n = cn.shape[-1]
+    sims = cn.size // (n * n)
+    _check(lib().orc_ch_adi_steps_cook(sims, n, dt, D, gamma, L, sigma, seed, step0, nsteps, _p(cn), _p(cm)))
+    return cn, cm
 
 
 # ----------------------------------------------------------------- error metrics

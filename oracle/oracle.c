@@ -12,7 +12,7 @@
  * and notation.  Indices are 0-based in code; comments quote the paper's
  * 1-based steps.  "P:<lines>" cites /root/reference/PAPER.md line numbers.
  *
- * Readings of the paper (r1..r21 in DESIGN.md §3) used here:
+ * Readings of the paper (r1..r27 in DESIGN.md §3) used here:
  *   r4  4th-difference stencil is (1,-4,6,-4,1)/dx^4 (P:321 printed wrong)
  *   r5  the explicit grad^4 Cbar term of Eq 3.1 carries D*gamma
  *   r6  Cbar^{n+1} = 2C^n - C^{n-1}
@@ -582,5 +582,147 @@ int orc_ch1d_steps(int64_t n, int64_t m, double dt, double gam, double L, int64_
     }
     orc_cpenta_free(&cp);
     free(u); free(nl); free(f);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Coarsening statistics (thesis §7.1-7.5).                   */
+
+/* Free energy of P:819-825 (reading r24): the bulk term is 1/4 (C^2-1)^2,
+   whose derivative C^3 - C is the chemical potential of eq2:ch and whose
+   decay rate is the printed dF/dt = -int |grad(C^3 - C - gamma lap C)|^2
+   (the printed 1/2 (C^2-1)^2 would differentiate to 2(C^3 - C)):
+   F_h = dx^2 sum_ij [ 1/4 (C_ij^2 - 1)^2
+                       + 1/2 gamma ((C_{i+1,j} - C_ij)^2 + (C_{i,j+1} - C_ij)^2) / dx^2 ]
+   with periodic forward differences.  One value per simulation.             */
+int orc_ch_free_energy(int64_t sims, int64_t n, double L, double gam, const double *c, double *F)
+{
+    if (n < 2 || sims < 0) return ORC_EINVAL;
+    double dx = L / (double)n; /* r1 */
+    for (int64_t s = 0; s < sims; s++) {
+        const double *C = c + s * n * n;
+        double acc = 0.0;
+        for (int64_t j = 0; j < n; j++)
+            for (int64_t i = 0; i < n; i++) {
+                double v = C[j * n + i];
+                double gx = (C[j * n + (i + 1) % n] - v) / dx;
+                double gy = (C[((j + 1) % n) * n + i] - v) / dx;
+                acc += 0.25 * (v * v - 1.0) * (v * v - 1.0) + 0.5 * gam * (gx * gx + gy * gy);
+            }
+        F[s] = acc * dx * dx;
+    }
+    return ORC_OK;
+}
+
+/* The growth rate beta = -(t/F) dF/dt of P:3576 from samples F(t_k) of one
+   simulation (reading r27: central differences in t at interior samples,
+   one-sided at the two ends).  F, beta: [nt][sims].                         */
+int orc_coarsening_beta(int64_t nt, int64_t sims, const double *t, const double *F, double *beta)
+{
+    if (nt < 2 || sims < 0) return ORC_EINVAL;
+    for (int64_t k = 0; k < nt; k++) {
+        int64_t a = k > 0 ? k - 1 : 0, b = k < nt - 1 ? k + 1 : nt - 1;
+        for (int64_t s = 0; s < sims; s++) {
+            double dFdt = (F[b * sims + s] - F[a * sims + s]) / (t[b] - t[a]);
+            beta[k * sims + s] = -(t[k] / F[k * sims + s]) * dFdt;
+        }
+    }
+    return ORC_OK;
+}
+
+/* Counter-based normals for the Cahn–Hilliard–Cook noise (reading r26): the
+   thesis draws uniforms and applies Box–Muller; the generator
+   is unspecified, so both sides use this one.  splitmix64 finaliser chained
+   over (seed, step, sim, cell); two uniforms in (0,1) from two counters;
+   Box–Muller gives rho_x (cos branch) and rho_y (sin branch) of one cell.  */
+static uint64_t orc_mix64(uint64_t z)
+{
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+void orc_cook_rho(uint64_t seed, int64_t step, int64_t sim, int64_t cell, double *rx, double *ry)
+{
+    uint64_t k = orc_mix64(orc_mix64(orc_mix64(seed) ^ (uint64_t)step) ^ (uint64_t)sim);
+    uint64_t h1 = orc_mix64(k ^ (2 * (uint64_t)cell)), h2 = orc_mix64(k ^ (2 * (uint64_t)cell + 1));
+    double u1 = ((double)(h1 >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    double u2 = ((double)(h2 >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    double r = sqrt(-2.0 * log(u1)), th = 2.0 * 3.14159265358979323846 * u2;
+    *rx = r * cos(th);
+    *ry = r * sin(th);
+}
+
+/* eta_ij = sqrt(sigma / (dx^2 dt)) (div rho)_ij, the divergence
+   by periodic central differences (reading r26):
+   (div rho)_ij = (rho_x[i+1,j] - rho_x[i-1,j] + rho_y[i,j+1] - rho_y[i,j-1]) / (2 dx). */
+int orc_cook_noise(int64_t sims, int64_t n, double dt, double L, double sigma, uint64_t seed, int64_t step,
+                   double *eta)
+{
+    if (n < 3 || sims < 0 || !(dt > 0)) return ORC_EINVAL;
+    double dx = L / (double)n, amp = sqrt(sigma / (dx * dx * dt));
+    int64_t np = n * n;
+    double *rx = malloc(sizeof(double) * np), *ry = malloc(sizeof(double) * np);
+    if (!rx || !ry) { free(rx); free(ry); return ORC_ENOMEM; }
+    for (int64_t s = 0; s < sims; s++) {
+        for (int64_t k = 0; k < np; k++) orc_cook_rho(seed, step, s, k, &rx[k], &ry[k]);
+        for (int64_t j = 0; j < n; j++)
+            for (int64_t i = 0; i < n; i++) {
+                int64_t ip = (i + 1) % n, im = (i + n - 1) % n, jp = (j + 1) % n, jm = (j + n - 1) % n;
+                double div = (rx[j * n + ip] - rx[j * n + im] + ry[jp * n + i] - ry[jm * n + i]) / (2.0 * dx);
+                eta[s * np + j * n + i] = amp * div;
+            }
+    }
+    free(rx); free(ry);
+    return ORC_OK;
+}
+
+/* nsteps of Eq 3.1 for the Cahn–Hilliard–Cook equation: the
+   noise of step step0 + k enters the RHS as + 2/3 dt eta^n (reading r25:
+   the BDF2 weight of every explicit term of Eq 3.1(a)); otherwise as
+   orc_ch_adi_steps.  sigma = 0 is orc_ch_adi_steps exactly.                 */
+int orc_ch_adi_steps_cook(int64_t sims, int64_t n, double dt, double D, double gam, double L, double sigma,
+                          uint64_t seed, int64_t step0, int64_t nsteps, double *cn, double *cm)
+{
+    if (n < 7 || sims < 0 || nsteps < 0) return ORC_EINVAL;
+    int64_t np = n * n;
+    double *eta = malloc(sizeof(double) * np * (sims > 0 ? sims : 1));
+    double *R = malloc(sizeof(double) * np * (sims > 0 ? sims : 1));
+    if (!eta || !R) { free(eta); free(R); return ORC_ENOMEM; }
+    double dx = L / (double)n;
+    double sig = (2.0 / 3.0) * D * gam * dt / (dx * dx * dx * dx);
+    double *a = malloc(sizeof(double) * n), *b = malloc(sizeof(double) * n),
+           *c = malloc(sizeof(double) * n), *d = malloc(sizeof(double) * n),
+           *e = malloc(sizeof(double) * n);
+    for (int64_t i = 0; i < n; i++) { a[i] = sig; b[i] = -4 * sig; c[i] = 1 + 6 * sig; d[i] = -4 * sig; e[i] = sig; }
+    orc_cpenta cp;
+    int rc = orc_cpenta_init(&cp, n, a, b, c, d, e, NULL);
+    free(a); free(b); free(c); free(d); free(e);
+    if (rc) { free(eta); free(R); return rc; }
+    double *row = malloc(sizeof(double) * n), *sol = malloc(sizeof(double) * n);
+    for (int64_t step = 0; step < nsteps; step++) {
+        orc_ch_rhs(sims, n, dt, D, gam, L, cn, cm, R);
+        orc_cook_noise(sims, n, dt, L, sigma, seed, step0 + step, eta);
+        for (int64_t k = 0; k < np * sims; k++) R[k] += (2.0 / 3.0) * dt * eta[k];
+        for (int64_t s = 0; s < sims; s++) {
+            double *Rs = R + s * np, *Cn = cn + s * np, *Cm = cm + s * np;
+            for (int64_t j = 0; j < n; j++) {
+                orc_cpenta_solve(&cp, Rs + j * n, sol);
+                memcpy(Rs + j * n, sol, sizeof(double) * n);
+            }
+            for (int64_t i = 0; i < n; i++) {
+                for (int64_t j = 0; j < n; j++) row[j] = Rs[j * n + i];
+                orc_cpenta_solve(&cp, row, sol);
+                for (int64_t j = 0; j < n; j++) Rs[j * n + i] = sol[j];
+            }
+            for (int64_t k = 0; k < np; k++) {
+                double cnew = 2.0 * Cn[k] - Cm[k] + Rs[k];
+                Cm[k] = Cn[k];
+                Cn[k] = cnew;
+            }
+        }
+    }
+    orc_cpenta_free(&cp);
+    free(eta); free(R); free(row); free(sol);
     return ORC_OK;
 }
