@@ -464,6 +464,36 @@ def bench_adi(args, rank, world, dev):
     }
 
 
+def bench_coarsen(args, dev):
+    """SURVEY §8(f)2 on the configs[3] batch: 512 Cahn–Hilliard–Cook sims at
+    512^2 from C = 0 (sigma = 1e-14), every step followed by the
+    on-device free energy of all sims (the F(t) series beta is built from)."""
+    import torch
+    import paper_2101_06550_b200 as pb
+
+    tdt = torch.float64 if args.dtype == "f64" else torch.float32
+    dt = synth.ch_dt(ADI_N, ADI_L)
+    st = pb.CHState(torch.zeros((ADI_SIMS, ADI_N, ADI_N), dtype=tdt, device=dev))
+    F = torch.empty((args.adi_steps, ADI_SIMS), dtype=torch.float64, device=dev)
+    pb.ch_adi_step_cook(st, dt, sigma=1e-14, seed=1, step0=0, L=ADI_L, nsteps=args.warmup)
+    torch.cuda.synchronize(dev)
+    e0, e1 = _ev(torch), _ev(torch)
+    e0.record()
+    for k in range(args.adi_steps):
+        pb.ch_adi_step_cook(st, dt, sigma=1e-14, seed=1, step0=args.warmup + k, L=ADI_L, nsteps=1)
+        pb.ch_free_energy(st, F[k], L=ADI_L)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / args.adi_steps
+    f0, f1 = F[0].mean().item(), F[-1].mean().item()
+    del st, F
+    torch.cuda.empty_cache()
+    return {"value": round(ADI_SIMS / (ms * 1e-3), 2), "unit": "sim-timesteps/s", "ms_per_step": round(ms, 4),
+            "config": {"workload": "SURVEY 8(f)2 on configs[3]: 512 CHC sims at 512^2 from C=0, sigma=1e-14, "
+                                   "free energy of every sim after every step", "dtype": args.dtype},
+            "mean_F_first_last": [f0, f1]}
+
+
 def bench_cfg3(args, dev):
     """configs[2]: one 1024^2 simulation (L = 8 pi), 1000 steps = 100 replays of a
     10-step CUDA graph (launch-latency bound: 4 launches per step)."""
@@ -604,6 +634,7 @@ def run_ours(args):
     sweep = _leg(bench_sweep, args, dev) if (not args.no_sweep and rank == 0) else None
     cfg3 = _leg(bench_cfg3, args, dev) if (not args.no_adi and rank == 0) else None
     ch1d = _leg(bench_ch1d, args, dev) if (not args.no_ch1d and rank == 0) else None
+    coarsen = _leg(bench_coarsen, args, dev) if (not args.no_adi and rank == 0) else None
     dist_adi = _leg(bench_dist_adi, args, rank, world, dev) if not args.no_dist else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -629,7 +660,7 @@ def run_ours(args):
                        "parallelism": f"independent batches x{world}"},
             "roofline": r["roofline"], "cpu_baseline": cpu, "e2e": r["e2e"], "gpu_launches": r["launches"],
             "clocks": r["clocks"], "residual": r["residual"], "sweep": sweep, "ch_adi": adi, "cfg3": cfg3,
-            "ch1d": ch1d, "dist_adi": dist_adi,
+            "ch1d": ch1d, "coarsen": coarsen, "dist_adi": dist_adi,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

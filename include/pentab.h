@@ -245,6 +245,47 @@ PB_API int ch_workspace_bytes(int64_t sims, int64_t n, int dtype, size_t *bytes)
 PB_API int ch_adi_step(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nsteps, void *stream);
 
 /* ------------------------------------------------------------------------
+ * Coarsening statistics (thesis §7.1-7.5, experiments on
+ * batches of CH / Cahn–Hilliard–Cook simulations).
+ *
+ * ch_adi_step_cook — nsteps of Eq 3.1 for the Cahn–Hilliard–Cook equation
+ * (P:4496-4509): as ch_adi_step, with the thermal noise
+ *   eta_ij = sqrt(sigma / (dx^2 dt)) (div rho)_ij
+ * added to the RHS as + 2/3 dt eta^n (reading r25).  rho = (rho_x, rho_y) is
+ * a fresh N(0,1) vector field every step: one Box–Muller pair per cell from
+ * two uniforms of the counter-based splitmix64 hash of (seed, step, sim,
+ * cell) (reading r26; the same generator as the CPU oracle's); the
+ * divergence by periodic central differences.  noise->step0 is the step
+ * index of the first of the nsteps (steps step0 .. step0+nsteps-1 draw
+ * distinct fields).  sigma = 0 is ch_adi_step exactly.
+ * Errors: as ch_adi_step; PB_EINVAL for sigma < 0.                        */
+typedef struct {
+    double sigma;     /* noise intensity (P:4509 uses 1e-14) */
+    uint64_t seed;
+    int64_t step0;
+} pb_ch_noise;
+PB_API int ch_adi_step_cook(pb_ch_state *s, double dt, const pb_ch_params *p, const pb_ch_noise *noise,
+                            int64_t nsteps, void *stream);
+
+/* ch_free_energy — F of P:819-825 per simulation, on the device (reading
+ * r24: bulk 1/4 (C^2-1)^2, the form the printed dF/dt belongs to):
+ *   F_h = dx^2 sum_ij [ 1/4 (C_ij^2 - 1)^2
+ *                       + 1/2 gamma ((C_{i+1,j}-C_ij)^2 + (C_{i,j+1}-C_ij)^2) / dx^2 ]
+ * periodic forward differences, dx = L/n, accumulated in fp64 in a fixed
+ * order (deterministic).  s: as ch_adi_step (reads s->c_cur only; uses no
+ * workspace); F: device, s->sims doubles, written.  p->D is unused.
+ * Errors: PB_EINVAL, PB_ECUDA.                                             */
+PB_API int ch_free_energy(const pb_ch_state *s, const pb_ch_params *p, double *F, void *stream);
+
+/* ch_coarsening_beta — the growth rate beta = -(t/F) dF/dt of nt
+ * samples F[k][sim] taken at times t[k] (reading r27: central differences in
+ * t, one-sided at the two ends).  t: device, nt doubles, increasing; F, beta:
+ * device, nt*sims doubles.  The thesis then keeps 10 < t < 100, beta < 1
+ * (P:3580-3581).  Errors: PB_EINVAL (nt < 2), PB_ECUDA.                   */
+PB_API int ch_coarsening_beta(int64_t nt, int64_t sims, const double *t, const double *F, double *beta,
+                              void *stream);
+
+/* ------------------------------------------------------------------------
  * ch1d_step — nsteps of the batched 1D Cahn–Hilliard scheme, thesis §6.2
  * (eq6:1Dnumerical):
  *   (I + dt gamma d_xxxx) C^{n+1} = C^n + dt d_xx (C^3 - C)^n,  D = 1,

@@ -23,7 +23,8 @@ PB_NONPERIODIC, PB_PERIODIC = 0, 1
 # every symbol include/pentab.h declares
 EXPORTS = ("pent_factor", "pent_solve", "pent_solve_many", "pent_solve_strided", "pent_solve_info", "pent_refactor", "pent_factor_uniform",
            "pent_destroy", "tri_factor", "tri_solve", "tri_solve_strided", "tri_refactor", "tri_factor_uniform",
-           "tri_destroy", "stencil_apply", "ch_workspace_bytes", "ch_adi_step", "ch1d_step", "ch_dist_pass_a",
+           "tri_destroy", "stencil_apply", "ch_workspace_bytes", "ch_adi_step", "ch_adi_step_cook", "ch_free_energy",
+           "ch_coarsening_beta", "ch1d_step", "ch_dist_pass_a",
            "ch_dist_pack", "ch_dist_ysweep", "ch_dist_combine", "pb_last_error", "pb_launch_count", "pb_reset_launch_count",
            "pb_device_ok")
 
@@ -54,6 +55,10 @@ class pb_ch_state(ctypes.Structure):
 
 class pb_ch_params(ctypes.Structure):
     _fields_ = [("D", ctypes.c_double), ("gamma", ctypes.c_double), ("L", ctypes.c_double)]
+
+
+class pb_ch_noise(ctypes.Structure):
+    _fields_ = [("sigma", ctypes.c_double), ("seed", ctypes.c_uint64), ("step0", ctypes.c_int64)]
 
 
 class pb_ch1d_state(ctypes.Structure):
@@ -94,6 +99,10 @@ def lib() -> ctypes.CDLL:
         L.ch_workspace_bytes.argtypes = [I64, I64, I, ctypes.POINTER(ctypes.c_size_t)]
         L.ch_adi_step.argtypes = [ctypes.POINTER(pb_ch_state), D, ctypes.POINTER(pb_ch_params), I64, P]
         L.ch1d_step.argtypes = [ctypes.POINTER(pb_ch1d_state), D, ctypes.POINTER(pb_ch1d_params), I64, P]
+        L.ch_adi_step_cook.argtypes = [ctypes.POINTER(pb_ch_state), D, ctypes.POINTER(pb_ch_params),
+                                       ctypes.POINTER(pb_ch_noise), I64, P]
+        L.ch_free_energy.argtypes = [ctypes.POINTER(pb_ch_state), ctypes.POINTER(pb_ch_params), P, P]
+        L.ch_coarsening_beta.argtypes = [I64, I64, P, P, P, P]
         L.ch_dist_pass_a.argtypes = [I64, I64, I, P, P, P, D, ctypes.POINTER(pb_ch_params), P]
         L.ch_dist_pack.argtypes = [I64, I64, I64, P, P, P]
         L.ch_dist_ysweep.argtypes = [I64, I64, P, D, ctypes.POINTER(pb_ch_params), P]
@@ -308,6 +317,29 @@ def ch_adi_step(state: CHState, dt, *, D=1.0, gamma=0.01, L, nsteps=1, stream=No
     p = pb_ch_params(D, gamma, L)
     _check(lib().ch_adi_step(ctypes.byref(state.state), dt, ctypes.byref(p), nsteps, _stream(state.bufs[0], stream)))
     return state
+
+
+def ch_adi_step_cook(state: CHState, dt, *, sigma, seed, step0=0, D=1.0, gamma=0.01, L, nsteps=1, stream=None):
+    """nsteps of the Cahn–Hilliard–Cook equation on device."""
+    p = pb_ch_params(D, gamma, L)
+    nz = pb_ch_noise(sigma, seed, step0)
+    _check(lib().ch_adi_step_cook(ctypes.byref(state.state), dt, ctypes.byref(p), ctypes.byref(nz), nsteps,
+                                  _stream(state.bufs[0], stream)))
+    return state
+
+
+def ch_free_energy(state: CHState, F, *, gamma=0.01, L, stream=None):
+    """F (reading r24) of every simulation into the device tensor F."""
+    p = pb_ch_params(1.0, gamma, L)
+    _check(lib().ch_free_energy(ctypes.byref(state.state), ctypes.byref(p), _ptr(F), _stream(state.bufs[0], stream)))
+    return F
+
+
+def ch_coarsening_beta(t, F, beta, stream=None):
+    """beta = -(t/F) dF/dt (reading r27); t [nt], F and beta [nt][sims], device."""
+    nt = t.shape[0]
+    _check(lib().ch_coarsening_beta(nt, F.numel() // nt, _ptr(t), _ptr(F), _ptr(beta), _stream(F, stream)))
+    return beta
 
 
 class CH1DState:

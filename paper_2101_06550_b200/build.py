@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpentab.so")
-SOURCES = ["api.cu", "banded.cu", "banded_inst_f64_k2.cu", "banded_inst_f64_k1.cu", "banded_inst_f32_k2.cu", "banded_inst_f32_k1.cu", "stencil.cu", "ch_adi.cu", "fused_solve.cu", "fused_part_f64_inter.cu", "fused_part_f64_contig.cu", "fused_part_f32_inter.cu", "fused_part_f32_contig.cu", "ch1d.cu"]
+SOURCES = ["api.cu", "banded.cu", "banded_inst_f64_k2.cu", "banded_inst_f64_k1.cu", "banded_inst_f32_k2.cu", "banded_inst_f32_k1.cu", "stencil.cu", "ch_adi.cu", "fused_solve.cu", "fused_part_f64_inter.cu", "fused_part_f64_contig.cu", "fused_part_f32_inter.cu", "fused_part_f32_contig.cu", "ch1d.cu", "coarsen.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

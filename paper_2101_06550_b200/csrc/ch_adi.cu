@@ -49,10 +49,35 @@ __device__ __forceinline__ int64_t wrapi(int64_t x, int64_t n)
 // ext = 0: whole periodic grids [sim][n][n]; ext = 1: one row block of `rows`
 // rows in an extended (rows + 4) x n buffer (2 halo rows above and below,
 // configs[4]), periodic in i only
-template <typename TS>
+// Cahn–Hilliard–Cook noise (ch_adi_step_cook, readings r25/r26): the
+// counter-based N(0,1) pair (rho_x, rho_y) of one cell -- splitmix64 over
+// (seed, step, sim, cell), two uniforms in (0,1), Box–Muller.
+struct CookArgs {
+    double k_noise;   // 2/3 dt sqrt(sigma / (dx^2 dt)) / (2 dx); 0 = no noise
+    uint64_t key;     // mix(mix(seed) ^ step) (the sim is mixed in per CTA)
+};
+__host__ __device__ __forceinline__ uint64_t cook_mix(uint64_t z)
+{
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ void cook_rho(uint64_t k, uint64_t cell, double &rx, double &ry)
+{
+    const uint64_t h1 = cook_mix(k ^ (2 * cell)), h2 = cook_mix(k ^ (2 * cell + 1));
+    const double u1 = ((double)(h1 >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    const double u2 = ((double)(h2 >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    const double r = sqrt(-2.0 * log(u1)), th = 2.0 * 3.14159265358979323846 * u2;
+    rx = r * cos(th);
+    ry = r * sin(th);
+}
+constexpr int RN_I = RT_I + 2, RN_J = RT_J + 2;   // cells of the staged noise field (1-cell halo)
+
+template <typename TS, bool NOISE>
 __global__ void __launch_bounds__(RT_I) adi_rhs_kernel(const TS *__restrict__ cn, const TS *__restrict__ cm,
                                                        double *__restrict__ R, int64_t n, int64_t rows, int ext,
-                                                       double k_dif, double k_bih, double k_lap)
+                                                       double k_dif, double k_bih, double k_lap, CookArgs ck)
 {
     extern __shared__ __align__(16) double rhs_smem[];
     double(*sb)[RS_I] = reinterpret_cast<double(*)[RS_I]>(rhs_smem);                 // Cbar
@@ -86,6 +111,16 @@ __global__ void __launch_bounds__(RT_I) adi_rhs_kernel(const TS *__restrict__ cn
                 (&sb[0][0])[e] = 2.0 * x - y;
                 (&sc[0][0])[e] = x;
             }
+        }
+    }
+    double *nx = rhs_smem + 2 * RS_J * RS_I, *ny = nx + RN_J * RN_I;   // NOISE: rho_x, rho_y
+    if (NOISE) {
+        // one Box–Muller pair per cell of the tile and its 1-cell halo (periodic)
+        const uint64_t k = cook_mix(ck.key ^ (uint64_t)blockIdx.z);
+        for (int e = threadIdx.x; e < RN_J * RN_I; e += RT_I) {
+            const int r = e / RN_I, q = e % RN_I;
+            const int64_t jj = wrapi(j0 - 1 + r, n), ii = wrapi(i0 - 1 + q, n);
+            cook_rho(k, (uint64_t)(jj * n + ii), nx[e], ny[e]);
         }
     }
     __syncthreads();
@@ -122,7 +157,13 @@ __global__ void __launch_bounds__(RT_I) adi_rhs_kernel(const TS *__restrict__ cn
                            2.0 * ((b1[1] + b1[3]) + (bp1[1] + bp1[3])) + ((b0[0] + b0[4]) + (b2[2] + bp2[2]));
         const double lap = (n0[0] + n0[2]) + (n1[1] + np1[1]) - 4.0 * n0[1];
         const double d = b0[2] - sc[jj + 2][c];   // C^n - C^{n-1} = Cbar - C^n
-        __stcg(Ro + (j0 + jj) * n + i, k_dif * d + k_bih * bih + k_lap * lap);
+        double rv = k_dif * d + k_bih * bih + k_lap * lap;
+        if (NOISE) {
+            // + 2/3 dt eta, eta = amp (div rho), central differences (r25, r26)
+            const int e = (jj + 1) * RN_I + (t + 1);
+            rv += ck.k_noise * ((nx[e + 1] - nx[e - 1]) + (ny[e + RN_I] - ny[e - RN_I]));
+        }
+        __stcg(Ro + (j0 + jj) * n + i, rv);
 #pragma unroll
         for (int q = 0; q < 5; ++q) {
             b2[q] = b1[q];
@@ -202,21 +243,29 @@ static AdiCoef adi_coef(int64_t n, double dt, const pb_ch_params *p)
     return c;
 }
 
-template <typename TS>
-static int launch_rhs(const TS *cn, const TS *cm, double *R, int64_t n, int64_t rows, int64_t sims, int ext,
-                      const AdiCoef &c, cudaStream_t st)
+template <typename TS, bool NOISE>
+static int launch_rhs_t(const TS *cn, const TS *cm, double *R, int64_t n, int64_t rows, int64_t sims, int ext,
+                        const AdiCoef &c, const CookArgs &ck, cudaStream_t st)
 {
-    constexpr size_t smem = sizeof(double) * 2 * RS_J * RS_I;
+    constexpr size_t smem = sizeof(double) * (2 * RS_J * RS_I + (NOISE ? 2 * RN_J * RN_I : 0));
     static std::once_flag once;
     static cudaError_t attr = cudaSuccess;
     std::call_once(once, [] {
-        attr = cudaFuncSetAttribute(adi_rhs_kernel<TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = cudaFuncSetAttribute(adi_rhs_kernel<TS, NOISE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem);
     });
     if (attr != cudaSuccess) return set_error(PB_ECUDA, "adi_rhs_kernel smem attribute: %s", cudaGetErrorString(attr));
     dim3 grid((unsigned)((n + RT_I - 1) / RT_I), (unsigned)((rows + RT_J - 1) / RT_J), (unsigned)sims);
-    adi_rhs_kernel<TS><<<grid, RT_I, smem, st>>>(cn, cm, R, n, rows, ext, c.k_dif, c.k_bih, c.k_lap);
+    adi_rhs_kernel<TS, NOISE><<<grid, RT_I, smem, st>>>(cn, cm, R, n, rows, ext, c.k_dif, c.k_bih, c.k_lap, ck);
     PB_LAUNCH_CHECK();
     return PB_OK;
+}
+template <typename TS>
+static int launch_rhs(const TS *cn, const TS *cm, double *R, int64_t n, int64_t rows, int64_t sims, int ext,
+                      const AdiCoef &c, cudaStream_t st, const CookArgs *ck = nullptr)
+{
+    if (ck && ck->k_noise != 0.0) return launch_rhs_t<TS, true>(cn, cm, R, n, rows, sims, ext, c, *ck, st);
+    return launch_rhs_t<TS, false>(cn, cm, R, n, rows, sims, ext, c, CookArgs{0.0, 0}, st);
 }
 
 template <typename TS>
@@ -229,7 +278,8 @@ static int launch_combine(int64_t count, const TS *cn, TS *cm, const double *v, 
 }
 
 template <typename TS>
-static int adi_run(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nsteps, cudaStream_t st)
+static int adi_run(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nsteps, cudaStream_t st,
+                   const pb_ch_noise *noise = nullptr)
 {
     const int64_t n = s->n, sims = s->sims, plane = n * n;
     const AdiCoef c = adi_coef(n, dt, p);
@@ -240,7 +290,13 @@ static int adi_run(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nst
     for (int64_t step = 0; step < nsteps; ++step) {
         const TS *cn = (const TS *)s->c_cur;
         TS *cm = (TS *)s->c_prev;
-        if ((rc = launch_rhs<TS>(cn, cm, w, n, n, sims, 0, c, st))) return rc;
+        CookArgs ck{0.0, 0};
+        if (noise && noise->sigma > 0) {
+            const double dx = p->L / (double)n;
+            ck.k_noise = (2.0 / 3.0) * dt * sqrt(noise->sigma / (dx * dx * dt)) / (2.0 * dx);
+            ck.key = cook_mix(cook_mix(noise->seed) ^ (uint64_t)(noise->step0 + step));
+        }
+        if ((rc = launch_rhs<TS>(cn, cm, w, n, n, sims, 0, c, st, &ck))) return rc;
         // x-sweep: systems = rows (sim, j), contiguous along i; y-sweep: systems =
         // columns i of each simulation, interleaved along j
         if ((rc = band_solve(h, w, PB_CONTIGUOUS, sims, plane, st))) return rc;
@@ -368,7 +424,23 @@ extern "C" int ch_workspace_bytes(int64_t sims, int64_t n, int dtype, size_t *by
     return PB_OK;
 }
 
+static int ch_adi_entry(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nsteps, void *stream,
+                        const pb_ch_noise *noise);
+
 extern "C" int ch_adi_step(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nsteps, void *stream)
+{
+    return ch_adi_entry(s, dt, p, nsteps, stream, nullptr);
+}
+
+extern "C" int ch_adi_step_cook(pb_ch_state *s, double dt, const pb_ch_params *p, const pb_ch_noise *noise,
+                                int64_t nsteps, void *stream)
+{
+    if (!noise || !(noise->sigma >= 0)) return pb::set_error(PB_EINVAL, "noise: sigma must be >= 0");
+    return ch_adi_entry(s, dt, p, nsteps, stream, noise);
+}
+
+static int ch_adi_entry(pb_ch_state *s, double dt, const pb_ch_params *p, int64_t nsteps, void *stream,
+                        const pb_ch_noise *noise)
 {
     using namespace pb;
     if (!s || !p) return set_error(PB_EINVAL, "null state/params");
@@ -385,5 +457,6 @@ extern "C" int ch_adi_step(pb_ch_state *s, double dt, const pb_ch_params *p, int
     if (!is_device_ptr(s->c_cur) || !is_device_ptr(s->c_prev) || !is_device_ptr(s->work))
         return set_error(PB_EINVAL, "ch_adi_step buffers must be device memory");
     cudaStream_t st = (cudaStream_t)stream;
-    return s->dtype == PB_F64 ? adi_run<double>(s, dt, p, nsteps, st) : adi_run<float>(s, dt, p, nsteps, st);
+    return s->dtype == PB_F64 ? adi_run<double>(s, dt, p, nsteps, st, noise)
+                              : adi_run<float>(s, dt, p, nsteps, st, noise);
 }
