@@ -340,8 +340,8 @@ def bench_penta(args, rank, world, dev):
     return {
         "value": value, "ms_per_step": ms / args.steps, "kern_ms": kern_ms_max, "launches": launches,
         "residual": res, "clocks": clk.summary(),
-        "roofline": roofline(alg_bytes, kern_ms_max * 1e-3, "fs_kernel (pent_solve, one launch: P1 + scan + P2)",
-                             f"pent_solve_{args.dtype}"),
+        "roofline": roofline(alg_bytes, kern_ms_max * 1e-3, "pent_solve: tp_p1_kernel -> tp_scan_kernel -> "
+                             "tp_p2_kernel (3 launches, PDL-chained)", f"pent_solve_{args.dtype}"),
         "e2e": {"value": round(e2e_val, 2), "unit": "Munknowns/s", "steps": e2e_steps,
                 "h2d_bytes_per_step": es * n * m, "d2h_bytes_per_step": es * n * m,
                 "path": "pent_solve(handle, host pinned rhs) -> pitched H2D | fused solve | D2H of 8 column "
@@ -458,8 +458,8 @@ def bench_adi(args, rank, world, dev):
                    "dtype": args.dtype},
         "launches": launches, "mean_abs_mass_drift_per_point": drift, "clocks": clk.summary(),
         "roofline": roofline(sum_over_ranks(alg_bytes, dev) / world, ms / steps * 1e-3,
-                             "one step: adi_rhs_kernel + fs_kernel<contiguous> + fs_kernel<interleaved> + "
-                             "adi_combine_kernel", f"adi_step_{args.dtype}",
+                             "one step: adi_rhs_kernel + fh_kernel<contiguous> (x-sweep) + fh_kernel<interleaved> "
+                             "(y-sweep) + adi_combine_kernel", f"adi_step_{args.dtype}",
                              "algorithmic 56 B/point (7 field passes); this schedule moves 11 fp64-sized passes"),
     }
 
@@ -559,7 +559,7 @@ def bench_ch1d(args, dev):
     return {"value": round(steps / (ms * 1e-3), 2), "unit": "batch-timesteps/s",
             "system_steps_per_s": round(CH1D_M * steps / (ms * 1e-3), 1), "ms_per_step": round(ms / steps, 4),
             "config": {"workload": "thesis §6.2.3: 2^20 1D CH systems x N=256, L=2pi, dt=0.1dx", "dtype": args.dtype},
-            "roofline": roofline(alg, ms / steps * 1e-3, "fs_kernel<MODE_CH1D> (RHS formed on chip, one launch per step)",
+            "roofline": roofline(alg, ms / steps * 1e-3, "fh_kernel<MODE_CH1D> (RHS formed on chip, one launch per step)",
                                  f"ch1d_{args.dtype}")}
 
 

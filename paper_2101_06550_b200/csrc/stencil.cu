@@ -10,6 +10,8 @@
 // a 180 GB B200 holds every grid of this workload resident.
 #include <string.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace pb {
@@ -81,8 +83,14 @@ extern "C" int stencil_apply(const pb_grid *g, const void *in, void *out, const 
 {
     using namespace pb;
     if (!g || !w || !weights || !in || !out) return set_error(PB_EINVAL, "null argument");
-    if (in == out) return set_error(PB_EINVAL, "in and out must differ (P:909)");
     if (g->dtype != PB_F64 && g->dtype != PB_F32) return set_error(PB_EINVAL, "bad dtype");
+    {
+        // the output must not overlap the input anywhere (separate buffers)
+        const size_t nb = dtype_size(g->dtype) * (size_t)(g->batch > 0 ? g->batch : 0) * (size_t)g->ny * (size_t)g->nx;
+        const uintptr_t a0 = (uintptr_t)in, b0 = (uintptr_t)out;
+        if (in == out || (nb > 0 && a0 < b0 + nb && b0 < a0 + nb))
+            return set_error(PB_EINVAL, "in and out must not overlap (P:909)");
+    }
     if (w->left < 0 || w->right < 0 || w->top < 0 || w->bottom < 0) return set_error(PB_EINVAL, "negative extent");
     const int wx = w->left + w->right + 1, wy = w->top + w->bottom + 1;
     if (wx > ST_MAXW || wy > ST_MAXW) return set_error(PB_EINVAL, "window larger than 15 x 15");
@@ -111,12 +119,19 @@ extern "C" int stencil_apply(const pb_grid *g, const void *in, void *out, const 
     if ((rc = so.in(out, bytes, st, true))) return rc;
     so.out_to(out);
     const size_t smem = es * (size_t)(ST_TX + wx - 1) * (ST_TY + wy - 1);
-    dim3 grid((unsigned)((g->nx + ST_TX - 1) / ST_TX), (unsigned)((g->ny + ST_TY - 1) / ST_TY), (unsigned)g->batch);
-    if (g->dtype == PB_F64)
-        stencil_kernel<double><<<grid, ST_NT, smem, st>>>((const double *)si.dev, (double *)so.dev, A);
-    else
-        stencil_kernel<float><<<grid, ST_NT, smem, st>>>((const float *)si.dev, (float *)so.dev, A);
-    PB_LAUNCH_CHECK();
+    // grid z is capped at 65535: launch the batch in slices
+    const size_t plane = es * (size_t)g->ny * (size_t)g->nx;
+    for (int64_t b0 = 0; b0 < g->batch; b0 += 65535) {
+        const int64_t nbz = std::min<int64_t>(65535, g->batch - b0);
+        dim3 grid((unsigned)((g->nx + ST_TX - 1) / ST_TX), (unsigned)((g->ny + ST_TY - 1) / ST_TY), (unsigned)nbz);
+        const char *src = (const char *)si.dev + plane * (size_t)b0;
+        char *dst = (char *)so.dev + plane * (size_t)b0;
+        if (g->dtype == PB_F64)
+            stencil_kernel<double><<<grid, ST_NT, smem, st>>>((const double *)src, (double *)dst, A);
+        else
+            stencil_kernel<float><<<grid, ST_NT, smem, st>>>((const float *)src, (float *)dst, A);
+        PB_LAUNCH_CHECK();
+    }
     if ((rc = si.finish())) return rc;
     return so.finish();
 }

@@ -22,7 +22,7 @@ def relerr(x, ref):
 
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-@pytest.mark.parametrize("sims,n", [(3, 100), (2, 512), (1, 7)])
+@pytest.mark.parametrize("sims,n", [(3, 100), (2, 512), (1, 9)])
 def test_free_energy_parity(sims, n, dtype):
     L, g = n * synth.DX_STATS, 0.01
     c = synth.ch_ic_random(sims, n, seed=21, lo=-1.1, hi=1.1)

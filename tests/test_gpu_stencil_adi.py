@@ -171,3 +171,11 @@ def test_adi_16384_single_grid():
     gn, gm = gpu_adi(c0, 1, dt=dt, L=L)
     assert relerr(gn, rn) <= 1e-12
     assert np.array_equal(gm, c0)
+
+
+def test_stencil_rejects_partial_overlap():
+    """Overlapping (not only identical) in/out ranges are rejected."""
+    x = torch.zeros(2, 8, 8, dtype=torch.float64, device="cuda")
+    with pytest.raises(pb.PentabError) as ei:
+        pb.stencil_apply(x[0:1], x.view(-1)[32:96].view(1, 8, 8), np.ones(3), left=1, right=1, top=0, bottom=0)
+    assert ei.value.code == pb.PB_EINVAL
