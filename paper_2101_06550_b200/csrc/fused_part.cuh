@@ -329,28 +329,28 @@ struct TpCfg {
     static constexpr int NC2 = sizeof(T) == 8 ? TP_NC2_64 : TP_NC2_32, R2 = sizeof(T) == 8 ? TP_R2_64 : TP_R2_32;
 };
 
-template <typename T, int K, bool PER>
+template <typename T, int K, bool PER, int LAY>
 static int tp_launch_t(const Band *h, T *x, int64_t count, int64_t bstride, cudaStream_t st, int64_t Mo, int64_t pitch)
 {
     constexpr int NC = TpCfg<T>::NC1, R = TpCfg<T>::R1, NC2 = TpCfg<T>::NC2, R2 = TpCfg<T>::R2;
-    auto k1 = tp::tp_p1_kernel<T, K, PER, NC, R>;
-    auto k2 = tp::tp_p2_kernel<T, K, PER, NC2, R2>;
+    auto k1 = tp::tp_p1_kernel<T, K, PER, NC, R, LAY>;
+    auto k2 = tp::tp_p2_kernel<T, K, PER, NC2, R2, LAY>;
     auto ks = tp::tp_scan_kernel<T, K, PER>;
     const size_t sm1 = sizeof(tp::P1Smem<T, NC, R>) + 1024;
     const size_t sm2 = sizeof(tp::P2Smem<T, NC2, R2>) + 1024;
     const size_t sms = (sizeof(tp::ScanSmem<T>) + 15) / 16 * 16 + sizeof(T) * 12 * (size_t)h->fplan.nq;
-    if (h->fplan.nq > tp::SL * tp::SEGMAX) return PB_EUNSUPPORTED;   // longer systems: the global kernel serves
+    if (h->fplan.nq > tp::SL * tp::NSEG) return PB_EUNSUPPORTED;   // longer systems: the global kernel serves
     static std::once_flag once;
     static cudaError_t attr = cudaSuccess;
     std::call_once(once, [&] {
         attr = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-        if (attr == cudaSuccess) attr = cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (attr == cudaSuccess) attr = cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         if (attr == cudaSuccess) attr = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
         cudaGetLastError();
     });
     if (attr != cudaSuccess) return set_error(PB_ECUDA, "tp kernels smem attribute: %s", cudaGetErrorString(attr));
     const int64_t M = Mo > 0 ? Mo : h->batch, n = h->n;
-    const int64_t P = pitch > 0 ? pitch : M;
+    const int64_t P = pitch > 0 ? pitch : (LAY == fs::LAY_CONTIG ? n : M);
     const int nq = h->fplan.nq;
     const int64_t Gb = (M + fs::TW - 1) / fs::TW, G = Gb * count;
     if (G > (1 << 30)) return PB_EUNSUPPORTED;
@@ -379,7 +379,7 @@ static int tp_launch_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
     }
     {
         bool flat = false;
-        int rc = tensor_map_for<T, fs::LAY_INTER>(S, x, M, n, count, bstride, P, &tmap, &flat);
+        int rc = tensor_map_for<T, LAY>(S, x, M, n, count, bstride, P, &tmap, &flat);
         if (rc) return rc;
         A.flat = flat ? 1 : 0;
     }
@@ -396,7 +396,7 @@ static int tp_launch_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
     A.xl = (T *)(base + off_xl);
     A.n = n;
     A.M = M;
-    A.bstride = count > 1 ? bstride : P * n;
+    A.bstride = count > 1 ? bstride : P * (LAY == fs::LAY_CONTIG ? M : n);
     A.pitch = P;
     A.ntiles = ntiles;
     // the last ~48 MB of f that P1 reads stay in L2 for P2's first (reversed) tiles
@@ -417,7 +417,7 @@ static int tp_launch_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
     {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)G);
-        cfg.blockDim = dim3(32 * ((nq + tp::SL - 1) / tp::SL));
+        cfg.blockDim = dim3(32 * std::min(tp::SEGMAX, (nq + tp::SL - 1) / tp::SL));
         cfg.dynamicSmemBytes = sms;
         cfg.stream = st;
         cfg.attrs = pdl;
@@ -593,6 +593,14 @@ static int fs_launch_t(const Band *h, T *x, T *xout, double alpha, int64_t count
 }
 
 
+// the two-pass kernels unless the held-tile kernel keeps all its warps busy
+// (5 <= N/64 <= 8) or the batch is too small to stream (N/64 <= 4, fewer
+// than 32 K systems: one launch instead of three)
+static inline bool use_twopass(int nq, int64_t systems)
+{
+    return nq > fh::NW || (nq >= 2 && nq <= fh::NW / 2 && systems >= 32768);
+}
+
 template <typename T, int LAY>
 static int fs_launch_dl(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t st, int64_t M,
                         int64_t pitch)
@@ -600,16 +608,18 @@ static int fs_launch_dl(const Band *h, void *x, int64_t count, int64_t bstride, 
     T *X = (T *)x;
     using namespace fs;
     int rc;
-    // interleaved systems longer than one held-tile CTA (8 chunks): the
+    // systems longer than one held-tile CTA (8 chunks), either layout: the
     // two-pass kernels (P1 / scan / P2; measured 2.5x faster than the cluster
     // exchange of the held-tile kernel at N = M = 8192)
-    if (LAY == LAY_INTER && h->fplan.nq > fh::NW) {
+    // (and for N/64 <= 4 in the bandwidth regime: the held-tile CTA then runs
+    // at most half its warps; 2^20 x 256 fp64: 1.52 vs 1.80 ms)
+    if (use_twopass(h->fplan.nq, (M > 0 ? M : h->batch) * count)) {
         if (h->K == 2)
-            rc = h->periodic ? tp_launch_t<T, 2, true>(h, X, count, bstride, st, M, pitch)
-                             : tp_launch_t<T, 2, false>(h, X, count, bstride, st, M, pitch);
+            rc = h->periodic ? tp_launch_t<T, 2, true, LAY>(h, X, count, bstride, st, M, pitch)
+                             : tp_launch_t<T, 2, false, LAY>(h, X, count, bstride, st, M, pitch);
         else
-            rc = h->periodic ? tp_launch_t<T, 1, true>(h, X, count, bstride, st, M, pitch)
-                             : tp_launch_t<T, 1, false>(h, X, count, bstride, st, M, pitch);
+            rc = h->periodic ? tp_launch_t<T, 1, true, LAY>(h, X, count, bstride, st, M, pitch)
+                             : tp_launch_t<T, 1, false, LAY>(h, X, count, bstride, st, M, pitch);
         if (rc != PB_EUNSUPPORTED) return rc;
     }
     {
@@ -647,7 +657,7 @@ int FS_NAME(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t
 int FS_INFO_NAME(const Band *h, int64_t M, int64_t count, int *info)
 {
     int rc;
-    if (FS_LAY == fs::LAY_INTER && h->fplan.nq > fh::NW && h->fplan.nq <= tp::SL * tp::SEGMAX &&
+    if (use_twopass(h->fplan.nq, M * count) && h->fplan.nq <= tp::SL * tp::NSEG &&
         (int64_t)h->fplan.nq * ((M + fs::TW - 1) / fs::TW) * count < ((int64_t)1 << 31)) {
         // the two-pass kernels: no clusters; info[2] = CTAs of P1
         const int64_t nt = (int64_t)h->fplan.nq * ((M + fs::TW - 1) / fs::TW) * count;

@@ -183,15 +183,43 @@ __device__ __forceinline__ unsigned char *smem_base()
     return tp_smem + ((1024u - (su32(tp_smem) & 1023u)) & 1023u);
 }
 
-template <typename T>
+// The tile (chunk q of group g) into dst.  Interleaved: one TMA box (32
+// systems, 64 rows).  Contiguous (rows of a grid, the ADI x-sweep): Q/EB boxes
+// of (EB unknowns = 128 B, 32 systems), 128B-swizzled (fs::csw) so the lanes
+// read their own systems' unknown k conflict-free.
+template <typename T, int LAY>
+__device__ __forceinline__ void tile_box(const CUtensorMap *tm, const Args<T> &A, int64_t g, int q, T *dst,
+                                         uint64_t *bar, uint64_t pol, bool store)
+{
+    const int b = (int)(g / A.Gb), gl = (int)(g - (int64_t)b * A.Gb);
+    if (LAY == fs::LAY_CONTIG) {
+#pragma unroll
+        for (int bx = 0; bx < Q / fs::Sw<T>::EB; ++bx) {
+            T *d = dst + bx * TW * fs::Sw<T>::EB;
+            const int r = q * Q + bx * fs::Sw<T>::EB;
+            if (store) {
+                if (A.flat) fs::tma_store2(tm, r, (int)((int64_t)b * A.M + gl * TW), d);
+                else fs::tma_store3(tm, r, gl * TW, b, d);
+            } else {
+                if (A.flat) tma_load2(d, tm, r, (int)((int64_t)b * A.M + gl * TW), bar, pol);
+                else tma_load3(d, tm, r, gl * TW, b, bar, pol);
+            }
+        }
+    } else if (store) {
+        if (A.flat) fs::tma_store2(tm, gl * TW, (int)((int64_t)b * A.n + (int64_t)q * Q), dst);
+        else fs::tma_store3(tm, gl * TW, q * Q, b, dst);
+    } else {
+        if (A.flat) tma_load2(dst, tm, gl * TW, (int)((int64_t)b * A.n + (int64_t)q * Q), bar, pol);
+        else tma_load3(dst, tm, gl * TW, q * Q, b, bar, pol);
+    }
+}
+template <typename T, int LAY>
 __device__ __forceinline__ void issue_tile(const CUtensorMap *tm, const Args<T> &A, int64_t g, int q, T *dst,
                                            uint64_t *bar, const T *rows, uint32_t row_bytes, uint64_t pol,
                                            uint32_t extra_tx = 0)
 {
-    const int b = (int)(g / A.Gb), gl = (int)(g - (int64_t)b * A.Gb);
     bar_expect_tx(bar, (uint32_t)(Q * TW * sizeof(T)) + row_bytes + extra_tx);
-    if (A.flat) tma_load2(dst, tm, gl * TW, (int)((int64_t)b * A.n + (int64_t)q * Q), bar, pol);
-    else tma_load3(dst, tm, gl * TW, q * Q, b, bar, pol);
+    tile_box<T, LAY>(tm, A, g, q, dst, bar, pol, false);
     bulk_load(dst + Q * TW, rows, row_bytes, bar);
 }
 
@@ -203,7 +231,7 @@ constexpr int PD = 4;   // coefficient rows software-pipelined this many rows ah
 // (F0, F1, F2, Wa, Wb, 0) -> forward carry (y0, y1), functional (a0, a1); hist
 // = g of the last four rows swept (the cyclic rows are the last four of the
 // system, hence of their tile).  FULL: kmax == Q.
-template <typename T, int K, bool PER, bool FULL>
+template <typename T, int K, bool PER, bool FULL, int LAY>
 __device__ __forceinline__ void p1_tile(const T *d, const T *c, int lane, int kmax, T &y0, T &y1, T &a0, T &a1,
                                         T (&hist)[4])
 {
@@ -214,7 +242,7 @@ __device__ __forceinline__ void p1_tile(const T *d, const T *c, int lane, int km
         lds2(c + u * REC, cf[u][0], cf[u][1]);
         lds2(c + u * REC + 2, cf[u][2], cf[u][3]);
         lds2(c + u * REC + 4, cf[u][4], cf[u][5]);
-        vv[u] = d[u * TW + lane];
+        vv[u] = fs::tld<T, LAY>(d, u, lane);
     }
 #pragma unroll
     for (int kk = 0; kk < Q; ++kk) {
@@ -224,7 +252,7 @@ __device__ __forceinline__ void p1_tile(const T *d, const T *c, int lane, int km
             lds2(c + (kk + PD) * REC, cf[sl][0], cf[sl][1]);
             lds2(c + (kk + PD) * REC + 2, cf[sl][2], cf[sl][3]);
             lds2(c + (kk + PD) * REC + 4, cf[sl][4], cf[sl][5]);
-            vv[sl] = d[(kk + PD) * TW + lane];
+            vv[sl] = fs::tld<T, LAY>(d, kk + PD, lane);
         }
         if (FULL || kk < kmax) {
             T tt = f0 * v;
@@ -242,14 +270,15 @@ __device__ __forceinline__ void p1_tile(const T *d, const T *c, int lane, int km
 // ---------------------------------------------------------------- P1 (+ the group scans)
 template <typename T, int NC, int R>
 struct P1Smem {
-    static constexpr int SLOT = ((Q * TW + Q * REC) * (int)sizeof(T) + 127) / 128 * 128 / (int)sizeof(T);
+    // (1 KB multiples: the contiguous layout's 128B-swizzled boxes)
+    static constexpr int SLOT = ((Q * TW + Q * REC) * (int)sizeof(T) + 1023) / 1024 * 1024 / (int)sizeof(T);
     T slot[NC][R][SLOT];
     uint64_t full[NC][R];
 };
 
 // NC consumer warps stream the tiles; nothing waits on anything but its own
 // slot (no fences, no counters): the kernel boundary publishes the records.
-template <typename T, int K, bool PER, int NC, int R>
+template <typename T, int K, bool PER, int NC, int R, int LAY>
 __global__ void __launch_bounds__(32 * NC, 1) tp_p1_kernel(const __grid_constant__ CUtensorMap tmap, const Args<T> A)
 {
     using S = P1Smem<T, NC, R>;
@@ -268,7 +297,8 @@ __global__ void __launch_bounds__(32 * NC, 1) tp_p1_kernel(const __grid_constant
         const TC tc = tile_coords(A, t);
         uint64_t pol = pol_first;
         if (t >= A.keep_from) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-        issue_tile<T>(&tmap, A, tc.g, tc.q, sm.slot[w][r], &sm.full[w][r], A.rec + (int64_t)tc.q * Q * REC, rb, pol);
+        issue_tile<T, LAY>(&tmap, A, tc.g, tc.q, sm.slot[w][r], &sm.full[w][r], A.rec + (int64_t)tc.q * Q * REC, rb,
+                           pol);
     };
     if (lane == 0)
         for (int r = 0; r < R; ++r)
@@ -288,8 +318,8 @@ __global__ void __launch_bounds__(32 * NC, 1) tp_p1_kernel(const __grid_constant
         // zero-inflow forward sweep, carry and back-substitution functional
         T y0, y1, a0, a1;
         T hist[4] = {T(0), T(0), T(0), T(0)};
-        if (A.n - r0 >= Q) p1_tile<T, K, PER, true>(d, c, lane, Q, y0, y1, a0, a1, hist);
-        else p1_tile<T, K, PER, false>(d, c, lane, (int)(A.n - r0), y0, y1, a0, a1, hist);
+        if (A.n - r0 >= Q) p1_tile<T, K, PER, true, LAY>(d, c, lane, Q, y0, y1, a0, a1, hist);
+        else p1_tile<T, K, PER, false, LAY>(d, c, lane, (int)(A.n - r0), y0, y1, a0, a1, hist);
         TPQ(1);
         // every value read from the slot has been consumed by the sweep: the
         // slot can take its refill
@@ -332,12 +362,13 @@ __global__ void __launch_bounds__(32 * NC, 1) tp_p1_kernel(const __grid_constant
 // The same affine algebra as hold_scan (fused_hold.cuh); cyclic: the true g
 // on the four last rows and (x_0, x_1) = Z_{-1} give Navon's / Sherman–
 // Morrison's x_l.  A programmatic dependent of P1 (launches while P1 runs).
-constexpr int SL = 16;     // chunks per segment (warp)
-constexpr int SEGMAX = 8;  // warps per CTA (the full register budget each): nq <= 128
+constexpr int SL = 16;      // chunks per segment
+constexpr int SEGMAX = 8;   // warps per CTA (the full register budget each)
+constexpr int NSEG = 32;    // segments per group: nq <= 512 (a warp folds segments w, w + 8, ...)
 template <typename T>
 struct ScanSmem {
-    T a[SEGMAX][TW][2], b[SEGMAX][TW][2], ys[SEGMAX][TW][2];
-    T m[SEGMAX][12];         // P, Pb, Kc per segment
+    T a[NSEG][TW][2], b[NSEG][TW][2], ys[NSEG][TW][2];
+    T m[NSEG][12];          // P, Pb, Kc per segment
     T gv[4][TW];
     // followed by the chunk maps ct[nq][12]
 };
@@ -350,26 +381,23 @@ __global__ void __launch_bounds__(32 * SEGMAX, 1) tp_scan_kernel(const Args<T> A
     T *ctm = reinterpret_cast<T *>(tp_scan_smem + (sizeof(ScanSmem<T>) + 15) / 16 * 16);
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     for (int e = threadIdx.x; e < A.nq * 12; e += blockDim.x) ctm[e] = A.ct[e];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nseg = blockDim.x >> 5;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    const int nsg = (A.nq + SL - 1) / SL;
     const int64_t g = blockIdx.x;
-    const int c0 = w * SL, nc = max(0, min(SL, A.nq - c0));
-    T *cr = A.car + (g * A.nq + c0) * 4 * TW + lane;
-    int qs[4] = {-1, -1, -1, -1};
-    if (PER) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) qs[j] = A.srow[j] >= 0 ? (int)(A.srow[j] / Q) - c0 : -1;
-    }
+    T *cg0 = A.car + g * A.nq * 4 * TW + lane;
     __syncthreads();
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    T r[SL][4];
+    // ---- pass A: every segment of this warp with zero inflows
+    for (int sg = w; sg < nsg; sg += nwarp) {
+        const int c0 = sg * SL, nc = min(SL, A.nq - c0);
+        const T *cr = cg0 + (int64_t)c0 * 4 * TW;
+        T r[SL][4];
 #pragma unroll
-    for (int i = 0; i < SL; ++i)
-        if (i < nc) {
+        for (int i = 0; i < SL; ++i)
+            if (i < nc) {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) r[i][e] = __ldcg(cr + (i * 4 + e) * TW);
-        }
-    // ---- pass A
-    {
+                for (int e = 0; e < 4; ++e) r[i][e] = __ldcg(cr + (i * 4 + e) * TW);
+            }
         T y0 = T(0), y1 = T(0), b0 = T(0), b1 = T(0);
         T Ph[4] = {T(1), T(0), T(0), T(1)}, Qb[4] = {T(1), T(0), T(0), T(1)}, Kc[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
@@ -396,44 +424,52 @@ __global__ void __launch_bounds__(32 * SEGMAX, 1) tp_scan_kernel(const Args<T> A
                 fs::mmul(Qb, mb, Qb);
                 fs::mmul(mf, Ph, Ph);
             }
-        sm.a[w][lane][0] = y0, sm.a[w][lane][1] = y1;
-        sm.b[w][lane][0] = b0, sm.b[w][lane][1] = b1;
-        if (lane < 4) sm.m[w][lane] = Ph[lane], sm.m[w][4 + lane] = Qb[lane], sm.m[w][8 + lane] = Kc[lane];
+        sm.a[sg][lane][0] = y0, sm.a[sg][lane][1] = y1;
+        sm.b[sg][lane][0] = b0, sm.b[sg][lane][1] = b1;
+        if (lane < 4) sm.m[sg][lane] = Ph[lane], sm.m[sg][4 + lane] = Qb[lane], sm.m[sg][8 + lane] = Kc[lane];
     }
     __syncthreads();
     // ---- combine (warp 0): every segment's true inflows Y (forward) and Z
     // (from above) into shared memory, (x_0, x_1) = the outflow of segment 0
     if (w == 0) {
         T ya = T(0), yb = T(0);
-#pragma unroll
-        for (int v = 0; v < SEGMAX; ++v)
-            if (v < nseg) {
-                sm.ys[v][lane][0] = ya, sm.ys[v][lane][1] = yb;
-                T t0, t1;
-                fs::mv(sm.m[v], ya, yb, t0, t1);
-                ya = t0 + sm.a[v][lane][0];
-                yb = t1 + sm.a[v][lane][1];
-            }
+        for (int v = 0; v < nsg; ++v) {
+            sm.ys[v][lane][0] = ya, sm.ys[v][lane][1] = yb;
+            T t0, t1;
+            fs::mv(sm.m[v], ya, yb, t0, t1);
+            ya = t0 + sm.a[v][lane][0];
+            yb = t1 + sm.a[v][lane][1];
+        }
         T za = T(0), zb = T(0);
-#pragma unroll
-        for (int v = SEGMAX - 1; v >= 0; --v)
-            if (v < nseg) {
-                T t0, t1, u0, u1;
-                fs::mv(sm.m[v] + 4, za, zb, t0, t1);
-                fs::mv(sm.m[v] + 8, sm.ys[v][lane][0], sm.ys[v][lane][1], u0, u1);
-                sm.a[v][lane][0] = za, sm.a[v][lane][1] = zb;   // a[v] := Z above segment v
-                za = t0 + u0 + sm.b[v][lane][0];
-                zb = t1 + u1 + sm.b[v][lane][1];
-            }
+        for (int v = nsg - 1; v >= 0; --v) {
+            T t0, t1, u0, u1;
+            fs::mv(sm.m[v] + 4, za, zb, t0, t1);
+            fs::mv(sm.m[v] + 8, sm.ys[v][lane][0], sm.ys[v][lane][1], u0, u1);
+            sm.a[v][lane][0] = za, sm.a[v][lane][1] = zb;   // a[v] := Z above segment v
+            za = t0 + u0 + sm.b[v][lane][0];
+            zb = t1 + u1 + sm.b[v][lane][1];
+        }
         sm.b[0][lane][0] = za, sm.b[0][lane][1] = zb;   // b[0] := (x_0, x_1)
     }
     __syncthreads();
-    const T Y0 = sm.ys[w][lane][0], Y1 = sm.ys[w][lane][1], Z0 = sm.a[w][lane][0], Z1 = sm.a[w][lane][1];
     const T x0 = sm.b[0][lane][0], x1 = sm.b[0][lane][1];
-    // ---- pass B
-    T cz[SL][2];
-    {
-        T y0 = Y0, y1 = Y1;
+    // ---- pass B: the walks again from the true (Y, Z) of each of this warp's segments
+    for (int sg = w; sg < nsg; sg += nwarp) {
+        const int c0 = sg * SL, nc = min(SL, A.nq - c0);
+        T *cr = cg0 + (int64_t)c0 * 4 * TW;
+        int qs[4] = {-1, -1, -1, -1};
+        if (PER) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) qs[j] = A.srow[j] >= 0 ? (int)(A.srow[j] / Q) - c0 : -1;
+        }
+        T r[SL][4], cz[SL][2];
+#pragma unroll
+        for (int i = 0; i < SL; ++i)
+            if (i < nc) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) r[i][e] = __ldcg(cr + (i * 4 + e) * TW);
+            }
+        T y0 = sm.ys[sg][lane][0], y1 = sm.ys[sg][lane][1];
 #pragma unroll
         for (int i = 0; i < SL; ++i)
             if (i < nc) {
@@ -456,7 +492,7 @@ __global__ void __launch_bounds__(32 * SEGMAX, 1) tp_scan_kernel(const Args<T> A
                 r[i][0] = y0, r[i][1] = y1;
                 y0 = n0, y1 = n1;
             }
-        T z0 = Z0, z1 = Z1;
+        T z0 = sm.a[sg][lane][0], z1 = sm.a[sg][lane][1];
 #pragma unroll
         for (int i = SL - 1; i >= 0; --i)
             if (i < nc) {
@@ -504,13 +540,13 @@ template <typename T, int NC, int R>
 struct P2Smem {
     // tile | coefficient rows | the tile's inflows [4][TW] | x_l [2][TW]
     static constexpr int INF = Q * TW + Q * COEF_STRIDE, XL = INF + 4 * TW;
-    static constexpr int SLOT = ((XL + 2 * TW) * (int)sizeof(T) + 127) / 128 * 128 / (int)sizeof(T);
+    static constexpr int SLOT = ((XL + 2 * TW) * (int)sizeof(T) + 1023) / 1024 * 1024 / (int)sizeof(T);
     T slot[NC][R][SLOT];
     T cpriv[NC][Q * COEF_STRIDE];   // the current tile's coefficient rows (its slot is refilled early)
     uint64_t full[NC][R];
 };
 
-template <typename T, int K, bool PER, int NC, int R>
+template <typename T, int K, bool PER, int NC, int R, int LAY>
 __global__ void __launch_bounds__(32 * NC, 1) tp_p2_kernel(const __grid_constant__ CUtensorMap tmap, const Args<T> A)
 {
     using S = P2Smem<T, NC, R>;
@@ -535,8 +571,8 @@ __global__ void __launch_bounds__(32 * NC, 1) tp_p2_kernel(const __grid_constant
     };
     auto issue = [&](int64_t i, int r, bool with_in) {
         const TC tc = tile_coords(A, tile_of(i));
-        issue_tile<T>(&tmap, A, tc.g, tc.q, sm.slot[w][r], &sm.full[w][r], A.coef + (int64_t)tc.q * Q * COEF_STRIDE,
-                      rb, pol, ib + xb);
+        issue_tile<T, LAY>(&tmap, A, tc.g, tc.q, sm.slot[w][r], &sm.full[w][r],
+                           A.coef + (int64_t)tc.q * Q * COEF_STRIDE, rb, pol, ib + xb);
         if (with_in) issue_in(i, r);
     };
     // f and the coefficients are not written by P1 or the scan: the first
@@ -568,7 +604,7 @@ __global__ void __launch_bounds__(32 * NC, 1) tp_p2_kernel(const __grid_constant
         if (PER) xl0 = d[S::XL + lane], xl1 = d[S::XL + TW + lane];
         T v[Q];
 #pragma unroll
-        for (int kk = 0; kk < Q; ++kk) v[kk] = d[kk * TW + lane];
+        for (int kk = 0; kk < Q; ++kk) v[kk] = fs::tld<T, LAY>(d, kk, lane);
         {
             // the coefficient rows into the warp's private buffer (16-byte units)
             const float4 *src = reinterpret_cast<const float4 *>(d + Q * TW);
@@ -600,12 +636,11 @@ __global__ void __launch_bounds__(32 * NC, 1) tp_p2_kernel(const __grid_constant
         }
         T *dw = sm.slot[w][r];
 #pragma unroll
-        for (int kk = 0; kk < Q; ++kk) dw[kk * TW + lane] = v[kk];
+        for (int kk = 0; kk < Q; ++kk) fs::tst<T, LAY>(dw, kk, lane, v[kk]);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();   // (also: cp is rewritten by the next tile)
         if (lane == 0) {
-            if (A.flat) fs::tma_store2(&tmap, gl * TW, (int)((int64_t)b * A.n + r0), dw);
-            else fs::tma_store3(&tmap, gl * TW, (int)r0, b, dw);
+            tile_box<T, LAY>(&tmap, A, g, q, dw, nullptr, 0, true);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             if (i + R * NWT < A.ntiles) {
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");

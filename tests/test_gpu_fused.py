@@ -224,13 +224,12 @@ def test_host_buffer_pipelined(pinned):
 
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("n,sigma", [(3000, 45.09), (700, 68.0), (2000, 2700.0), (130, 2700.0), (8192, 45.09),
-                                     (12000, 45.09), (20000, 45.09)])
+                                     (12000, 45.09), (20000, 45.09), (40000, 45.09)])
 def test_cluster_and_global_paths(n, sigma, dtype):
     """The interleaved solve's kernels against the oracle: the held-tile kernel
     for N <= 8 chunks of 64 rows (n = 130), the two-pass streaming kernels for
-    8 < N/64 <= 128 (n = 700 .. 8192), the two-pass cluster kernel beyond
-    within its span (256 chunks fp32: n = 12000 fp32), the global-scan kernel
-    beyond that (n = 12000 fp64, n = 20000).
+    8 < N/64 <= 512 (n = 700 .. 20000; the scan folds up to 32 segments of 16
+    chunks), the global-scan kernel beyond (n = 40000).
     Cyclic (Navon), the thesis operators (sigma 45-68) and a slowly decaying
     one (sigma 2700: kappa 4.3e4), ragged n."""
     m = 200
@@ -242,7 +241,7 @@ def test_cluster_and_global_paths(n, sigma, dtype):
     nq = (n + 63) // 64
     if nq <= 8:             # held tiles: one chunk per consumer warp (8), one CTA per group
         assert kind == 2 and cs == 1 and cpc == nq and ncl >= 1, (cs, cpc, ncl, kind)
-    elif nq <= 128:         # two-pass streaming kernels
+    elif nq <= 512:         # two-pass streaming kernels
         assert kind == 3 and cs == 0 and ncl >= 1, (cs, cpc, ncl, kind)
     elif nq > (120 if dtype == "f64" else 256):   # CSMAX 8 x chunks per CTA (15 fp64, 32 fp32)
         assert cs == 0 and kind == 0
@@ -254,3 +253,24 @@ def test_cluster_and_global_paths(n, sigma, dtype):
     # kappa = 1 + 16 sigma = 4.3e4 at sigma 2700: fp32 is kappa-limited there (~1.7e-4 measured)
     tol = TOL[dtype] if sigma < 100 else (1e-12 if dtype == "f64" else 1e-3)
     assert relerr(x.double().cpu().numpy(), ref) <= tol
+
+
+@pytest.mark.parametrize("n,m,layout", [(256, 65536, "interleaved"), (200, 40000, "contiguous"), (128, 32768, "interleaved")])
+def test_twopass_short_systems_large_batch(n, m, layout):
+    """N/64 <= 4 with >= 32 K systems takes the two-pass kernels (the held-tile
+    CTA would idle half its warps); sampled systems against the oracle."""
+    s = synth.SIGMA_STATS
+    diags = synth.const_penta(n, s, -4 * s, 1 + 6 * s, -4 * s, s)
+    h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in diags], batch=m, n=n, periodic=True)
+    assert h.solve_info(layout)[3] == 3
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n)
+    f = torch.rand(n * m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    x = f.clone()
+    h.solve(x, layout=layout)
+    torch.cuda.synchronize()
+    F = f.view(n, m) if layout == "interleaved" else f.view(m, n).t()
+    X = x.view(n, m) if layout == "interleaved" else x.view(m, n).t()
+    for sy in (0, 31, 32, m // 2 + 7, m - 1):
+        ref = oracle.penta_batch_solve(*diags, F[:, sy].cpu().numpy().copy(), n=n, m=1, periodic=True)
+        assert relerr(X[:, sy].cpu().numpy(), ref) <= 1e-12, sy

@@ -1,7 +1,7 @@
 mkdir -p gpurun_out
 python -c "import torch; torch.zeros(1).cuda()"
 cp paper_2101_06550_b200/libpentab.so /tmp/orig.so
-for v in orig I J K; do
+for v in orig C M N; do
  if [ $v != orig ]; then cp tools/variants/v_$v.so paper_2101_06550_b200/libpentab.so; fi
  echo "== $v"
  timeout 200 python tools/fs_time.py f64 8192:8192 4096:4096 2048:2048 1024:262144 2>&1 | grep -v Warn
