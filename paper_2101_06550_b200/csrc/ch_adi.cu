@@ -68,16 +68,18 @@ __device__ __forceinline__ void cook_rho(uint64_t k, uint64_t cell, double &rx, 
     const uint64_t h1 = cook_mix(k ^ (2 * cell)), h2 = cook_mix(k ^ (2 * cell + 1));
     const double u1 = ((double)(h1 >> 11) + 0.5) * (1.0 / 9007199254740992.0);
     const double u2 = ((double)(h2 >> 11) + 0.5) * (1.0 / 9007199254740992.0);
-    const double r = sqrt(-2.0 * log(u1)), th = 2.0 * 3.14159265358979323846 * u2;
-    rx = r * cos(th);
-    ry = r * sin(th);
+    // cos / sin of 2 pi u2 (as the oracle) through sincospi: no argument reduction
+    const double r = sqrt(-2.0 * log(u1));
+    double sn, cs;
+    sincospi(2.0 * u2, &sn, &cs);
+    rx = r * cs;
+    ry = r * sn;
 }
-constexpr int RN_I = RT_I + 2, RN_J = RT_J + 2;   // cells of the staged noise field (1-cell halo)
 
-template <typename TS, bool NOISE>
+template <typename TS>
 __global__ void __launch_bounds__(RT_I) adi_rhs_kernel(const TS *__restrict__ cn, const TS *__restrict__ cm,
                                                        double *__restrict__ R, int64_t n, int64_t rows, int ext,
-                                                       double k_dif, double k_bih, double k_lap, CookArgs ck)
+                                                       double k_dif, double k_bih, double k_lap)
 {
     extern __shared__ __align__(16) double rhs_smem[];
     double(*sb)[RS_I] = reinterpret_cast<double(*)[RS_I]>(rhs_smem);                 // Cbar
@@ -111,16 +113,6 @@ __global__ void __launch_bounds__(RT_I) adi_rhs_kernel(const TS *__restrict__ cn
                 (&sb[0][0])[e] = 2.0 * x - y;
                 (&sc[0][0])[e] = x;
             }
-        }
-    }
-    double *nx = rhs_smem + 2 * RS_J * RS_I, *ny = nx + RN_J * RN_I;   // NOISE: rho_x, rho_y
-    if (NOISE) {
-        // one Box–Muller pair per cell of the tile and its 1-cell halo (periodic)
-        const uint64_t k = cook_mix(ck.key ^ (uint64_t)blockIdx.z);
-        for (int e = threadIdx.x; e < RN_J * RN_I; e += RT_I) {
-            const int r = e / RN_I, q = e % RN_I;
-            const int64_t jj = wrapi(j0 - 1 + r, n), ii = wrapi(i0 - 1 + q, n);
-            cook_rho(k, (uint64_t)(jj * n + ii), nx[e], ny[e]);
         }
     }
     __syncthreads();
@@ -157,13 +149,7 @@ __global__ void __launch_bounds__(RT_I) adi_rhs_kernel(const TS *__restrict__ cn
                            2.0 * ((b1[1] + b1[3]) + (bp1[1] + bp1[3])) + ((b0[0] + b0[4]) + (b2[2] + bp2[2]));
         const double lap = (n0[0] + n0[2]) + (n1[1] + np1[1]) - 4.0 * n0[1];
         const double d = b0[2] - sc[jj + 2][c];   // C^n - C^{n-1} = Cbar - C^n
-        double rv = k_dif * d + k_bih * bih + k_lap * lap;
-        if (NOISE) {
-            // + 2/3 dt eta, eta = amp (div rho), central differences (r25, r26)
-            const int e = (jj + 1) * RN_I + (t + 1);
-            rv += ck.k_noise * ((nx[e + 1] - nx[e - 1]) + (ny[e + RN_I] - ny[e - RN_I]));
-        }
-        __stcg(Ro + (j0 + jj) * n + i, rv);
+        __stcg(Ro + (j0 + jj) * n + i, k_dif * d + k_bih * bih + k_lap * lap);
 #pragma unroll
         for (int q = 0; q < 5; ++q) {
             b2[q] = b1[q];
@@ -175,6 +161,35 @@ __global__ void __launch_bounds__(RT_I) adi_rhs_kernel(const TS *__restrict__ cn
         for (int q = 0; q < 3; ++q) {
             n1[q] = n0[q];
             n0[q] = np1[q];
+        }
+    }
+}
+
+// R += 2/3 dt eta, eta_ij = sqrt(sigma/(dx^2 dt)) (div rho)_ij (readings r25,
+// r26): a CTA stages one Box–Muller pair per cell of its 32 x 32 tile and the
+// 1-cell halo (periodic) in shared memory -- 18 KB, so many CTAs per SM hide
+// the fp64 log / sincos latency -- then adds the central-difference
+// divergence to its outputs (R read and written once more: 16 B per point).
+constexpr int CK_T = 32, CK_H = CK_T + 2;
+__global__ void __launch_bounds__(256) cook_add_kernel(double *__restrict__ R, int64_t n, double k_noise, uint64_t key)
+{
+    __shared__ double nx[CK_H * CK_H], ny[CK_H * CK_H];
+    const int64_t i0 = (int64_t)blockIdx.x * CK_T, j0 = (int64_t)blockIdx.y * CK_T, sim = blockIdx.z;
+    const uint64_t k = cook_mix(key ^ (uint64_t)sim);
+    for (int e = threadIdx.x; e < CK_H * CK_H; e += blockDim.x) {
+        const int r = e / CK_H, q = e % CK_H;
+        const int64_t jj = wrapi(j0 - 1 + r, n), ii = wrapi(i0 - 1 + q, n);
+        cook_rho(k, (uint64_t)(jj * n + ii), nx[e], ny[e]);
+    }
+    __syncthreads();
+    double *Rs = R + sim * n * n;
+    for (int e = threadIdx.x; e < CK_T * CK_T; e += blockDim.x) {
+        const int r = e / CK_T, q = e % CK_T;
+        const int64_t j = j0 + r, i = i0 + q;
+        if (j < n && i < n) {
+            const int c = (r + 1) * CK_H + (q + 1);
+            double *p = Rs + j * n + i;
+            __stcg(p, __ldcg(p) + k_noise * ((nx[c + 1] - nx[c - 1]) + (ny[c + CK_H] - ny[c - CK_H])));
         }
     }
 }
@@ -243,29 +258,26 @@ static AdiCoef adi_coef(int64_t n, double dt, const pb_ch_params *p)
     return c;
 }
 
-template <typename TS, bool NOISE>
-static int launch_rhs_t(const TS *cn, const TS *cm, double *R, int64_t n, int64_t rows, int64_t sims, int ext,
-                        const AdiCoef &c, const CookArgs &ck, cudaStream_t st)
-{
-    constexpr size_t smem = sizeof(double) * (2 * RS_J * RS_I + (NOISE ? 2 * RN_J * RN_I : 0));
-    static std::once_flag once;
-    static cudaError_t attr = cudaSuccess;
-    std::call_once(once, [] {
-        attr = cudaFuncSetAttribute(adi_rhs_kernel<TS, NOISE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem);
-    });
-    if (attr != cudaSuccess) return set_error(PB_ECUDA, "adi_rhs_kernel smem attribute: %s", cudaGetErrorString(attr));
-    dim3 grid((unsigned)((n + RT_I - 1) / RT_I), (unsigned)((rows + RT_J - 1) / RT_J), (unsigned)sims);
-    adi_rhs_kernel<TS, NOISE><<<grid, RT_I, smem, st>>>(cn, cm, R, n, rows, ext, c.k_dif, c.k_bih, c.k_lap, ck);
-    PB_LAUNCH_CHECK();
-    return PB_OK;
-}
 template <typename TS>
 static int launch_rhs(const TS *cn, const TS *cm, double *R, int64_t n, int64_t rows, int64_t sims, int ext,
                       const AdiCoef &c, cudaStream_t st, const CookArgs *ck = nullptr)
 {
-    if (ck && ck->k_noise != 0.0) return launch_rhs_t<TS, true>(cn, cm, R, n, rows, sims, ext, c, *ck, st);
-    return launch_rhs_t<TS, false>(cn, cm, R, n, rows, sims, ext, c, CookArgs{0.0, 0}, st);
+    constexpr size_t smem = sizeof(double) * 2 * RS_J * RS_I;
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    std::call_once(once, [] {
+        attr = cudaFuncSetAttribute(adi_rhs_kernel<TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    if (attr != cudaSuccess) return set_error(PB_ECUDA, "adi_rhs_kernel smem attribute: %s", cudaGetErrorString(attr));
+    dim3 grid((unsigned)((n + RT_I - 1) / RT_I), (unsigned)((rows + RT_J - 1) / RT_J), (unsigned)sims);
+    adi_rhs_kernel<TS><<<grid, RT_I, smem, st>>>(cn, cm, R, n, rows, ext, c.k_dif, c.k_bih, c.k_lap);
+    PB_LAUNCH_CHECK();
+    if (ck && ck->k_noise != 0.0) {
+        dim3 g2((unsigned)((n + CK_T - 1) / CK_T), (unsigned)((n + CK_T - 1) / CK_T), (unsigned)sims);
+        cook_add_kernel<<<g2, 256, 0, st>>>(R, n, ck->k_noise, ck->key);
+        PB_LAUNCH_CHECK();
+    }
+    return PB_OK;
 }
 
 template <typename TS>
