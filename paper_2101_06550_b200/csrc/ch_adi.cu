@@ -37,7 +37,13 @@ namespace pb {
 // C^n with their 2-point halo are staged once in shared memory (fp64), then
 // thread = column slides down the rows with the 13-point / 5-point windows in
 // registers (one new Cbar row and one new C^3 - C row per output).  R is fp64.
-constexpr int RT_I = 128, RT_J = 32;
+#ifndef RHS_RT_J
+#define RHS_RT_J 16
+#endif
+#ifndef RHS_RT_I
+#define RHS_RT_I 128
+#endif
+constexpr int RT_I = RHS_RT_I, RT_J = RHS_RT_J;
 constexpr int RS_I = RT_I + 4, RS_J = RT_J + 4;
 
 __device__ __forceinline__ int64_t wrapi(int64_t x, int64_t n)
