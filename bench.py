@@ -385,6 +385,16 @@ def bench_sweep(args, dev):
                 e1.record(side)
                 side.synchronize()
             hot_us = e0.elapsed_time(e1) * 1e3 / (5 * K)
+            host_us = None
+            if n == SWEEP_N[0]:
+                # host side of a pent_solve: 200 back-to-back calls without a graph,
+                # wall clock (the C-ABI call, marshalling and 3 launches each)
+                torch.cuda.synchronize(dev)
+                w0 = time.perf_counter()
+                for _ in range(200):
+                    h.solve(x)
+                torch.cuda.synchronize(dev)
+                host_us = round((time.perf_counter() - w0) * 1e6 / 200, 2)
             cold = []
             for _ in range(10):
                 flush.zero_()
@@ -396,7 +406,7 @@ def bench_sweep(args, dev):
                 cold.append(c0.elapsed_time(c1) * 1e3)
             cold_us = statistics.median(cold)
             b = 2 * es * n * m
-            out.append({"N": n, "batch": m, "dtype": dt,
+            out.append({"N": n, "batch": m, "dtype": dt, **({"host_us_per_call": host_us} if host_us else {}),
                         "hot_us": round(hot_us, 2), "hot_Munknowns_s": round(n * m / hot_us, 1),
                         "hot_frac": round(b / (hot_us * 1e-6) / 1e9 / peak, 4),
                         "cold_us": round(cold_us, 2), "cold_Munknowns_s": round(n * m / cold_us, 1),

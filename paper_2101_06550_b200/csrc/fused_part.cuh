@@ -66,123 +66,6 @@ static int tensor_map_for(FusedScratch &S, T *x, int64_t M, int64_t n, int64_t c
     return PB_OK;
 }
 
-// ---------------------------------------------------------------- cluster kernel launcher
-// Cluster size CS and chunks per CTA cpc = ceil(nq / CS) <= CPC: the candidate
-// that keeps the most SMs busy over the batch's groups (waves of NCL clusters,
-// NCL from the occupancy API), preferring cpc >= 4 and then the smaller CS.
-// Returns PB_EUNSUPPORTED when no cluster size fits (the global kernel serves).
-template <typename T, int K, bool PER, int MODE, int LAY>
-static int fc_launch_t(const Band *h, T *x, T *xout, double alpha, int64_t count, int64_t bstride, cudaStream_t st,
-                       int64_t Mo, int64_t pitch, int *info = nullptr)
-{
-    using C = fc::CCfg<T, MODE>;
-    auto kern = fc::fc_kernel<T, K, PER, MODE, LAY>;
-    const size_t smem = sizeof(fc::CSmem<T, MODE>) + 1024;
-    static std::once_flag once;
-    static cudaError_t attr = cudaSuccess;
-    static int ncl_of[fc::CSMAX + 1];
-    std::call_once(once, [&] {
-        attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (attr == cudaSuccess) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaGetLastError();
-        for (int cs = 1; cs <= fc::CSMAX; cs *= 2) {
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3((unsigned)(cs * 16));
-            cfg.blockDim = dim3(fc::NTHREADS);
-            cfg.dynamicSmemBytes = smem;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = cs;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            cfg.attrs = at;
-            cfg.numAttrs = 1;
-            int ncl = 0;
-            if (attr == cudaSuccess && cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess) ncl = 0;
-            cudaGetLastError();
-            ncl_of[cs] = ncl;
-        }
-    });
-    if (attr != cudaSuccess) return PB_EUNSUPPORTED;   // the shared-memory plan does not fit: the global kernel serves
-    const int64_t M = Mo > 0 ? Mo : h->batch, n = h->n;
-    const int64_t P = pitch > 0 ? pitch : (LAY == fs::LAY_CONTIG ? n : M);
-    const int nq = h->fplan.nq;
-    const int64_t Gb = (M + fs::TW - 1) / fs::TW, G = Gb * count;
-    if (G > (1 << 30)) return PB_EUNSUPPORTED;
-    const int nsm = fs_sm_count();
-    int best_cs = 0, best_cpc = 0, best_ncl = 0;
-    double best = -1;
-    for (int cs = 1; cs <= fc::CSMAX; cs *= 2) {
-        const int cpc = (nq + cs - 1) / cs;
-        if (cpc > C::CPC || ncl_of[cs] < 1 || (cs > 1 && cpc * (cs - 1) >= nq)) continue;   // (every CTA owns chunks)
-        const int64_t ncl = std::min<int64_t>(ncl_of[cs], G);
-        const int64_t waves = (G + ncl - 1) / ncl;
-        double eff = (double)G / (double)(waves * ncl) * (double)(ncl * cs) / (double)nsm;
-        if (cpc < 4 && nq >= 4) eff *= 0.85;
-        if (eff > best * 1.01) {
-            best = eff;
-            best_cs = cs;
-            best_cpc = cpc;
-            best_ncl = (int)ncl;
-        }
-    }
-    if (info) {
-        info[0] = best_cs;
-        info[1] = best_cpc;
-        info[2] = best_ncl;
-        return PB_OK;
-    }
-    if (!best_cs) return PB_EUNSUPPORTED;
-
-    fc::CArgs<T> A;
-    CUtensorMap tmap;
-    {
-        std::lock_guard<std::mutex> lk(h->fplan.mu);
-        FusedScratch &S = h->fplan.scratch[st];
-        bool flat = false;
-        int rc = tensor_map_for<T, LAY>(S, x, M, n, count, bstride, P, &tmap, &flat);
-        if (rc) return rc;
-        A.flat = flat ? 1 : 0;
-    }
-    A.rec = (const T *)h->fplan.rec;
-    A.coef = (const T *)h->coef;
-    A.ct = (const T *)h->fplan.ct;
-    A.rsp = (const T *)h->fplan.rsp;
-    A.scal = h->scal;
-    A.x = x;
-    A.xout = xout;
-    A.alpha = (T)alpha;
-    A.n = n;
-    A.M = M;
-    A.bstride = count > 1 ? bstride : P * (LAY == fs::LAY_CONTIG ? M : n);
-    A.pitch = P;
-    for (int j = 0; j < 4; ++j) A.srow[j] = h->srow[j];
-    A.nq = nq;
-    A.count = (int)count;
-    A.Gb = (int)Gb;
-    A.G = (int)G;
-    A.cs = best_cs;
-    A.cpc = best_cpc;
-    A.ncl = best_ncl;
-    A.prof = nullptr;
-    A.dbg = 0;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(best_ncl * best_cs));
-    cfg.blockDim = dim3(fc::NTHREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = best_cs;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    PB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tmap, A));
-    PB_LAUNCH_CHECK();
-    return PB_OK;
-}
-
 // ---------------------------------------------------------------- held-tile kernel launcher
 // Cluster size CS = ceil(nq / NW) (one chunk per consumer warp), cpc =
 // ceil(nq / CS) chunks per CTA; clusters = the occupancy API's maximum (each
@@ -631,16 +514,7 @@ static int fs_launch_dl(const Band *h, void *x, int64_t count, int64_t bstride, 
                              : fh_launch_t<T, 1, false, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch);
         if (rc != PB_EUNSUPPORTED) return rc;
     }
-    {
-    if (h->K == 2)
-        rc = h->periodic ? fc_launch_t<T, 2, true, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch)
-                         : fc_launch_t<T, 2, false, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch);
-    else
-        rc = h->periodic ? fc_launch_t<T, 1, true, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch)
-                         : fc_launch_t<T, 1, false, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch);
-    if (rc != PB_EUNSUPPORTED) return rc;
-    }
-    // beyond the cluster's shared-memory span: the global-scan kernel
+    // beyond the two-pass scan's span (N/64 > 512): the global-scan kernel
     if (h->K == 2)
         return h->periodic ? fs_launch_t<T, 2, true, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch)
                            : fs_launch_t<T, 2, false, MODE_SOLVE, LAY>(h, X, X, 0.0, count, bstride, st, M, pitch);
@@ -678,27 +552,14 @@ int FS_INFO_NAME(const Band *h, int64_t M, int64_t count, int *info)
                          : fh_launch_t<FS_T, 1, false, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0,
                                                                                nullptr, M, 0, info);
     if (rc != PB_EUNSUPPORTED) return rc;
-    info[3] = 1;
-    if (h->K == 2)
-        rc = h->periodic ? fc_launch_t<FS_T, 2, true, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0,
-                                                                                 nullptr, M, 0, info)
-                           : fc_launch_t<FS_T, 2, false, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0,
-                                                                                  nullptr, M, 0, info);
-    else
-        rc = h->periodic ? fc_launch_t<FS_T, 1, true, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0,
-                                                                              nullptr, M, 0, info)
-                         : fc_launch_t<FS_T, 1, false, fs::MODE_SOLVE, FS_LAY>(h, nullptr, nullptr, 0.0, count, 0,
-                                                                               nullptr, M, 0, info);
-    if (info[0] == 0) info[3] = 0;
-    return rc;
+    info[0] = info[1] = info[2] = info[3] = 0;   // the global-scan kernel
+    return PB_OK;
 }
 
 #ifdef FS_CH1D_NAME
 int FS_CH1D_NAME(const Band *h, const void *c, void *cnew, double alpha, int64_t M, cudaStream_t st)
 {
     int rc = fh_launch_t<FS_T, 2, true, fs::MODE_CH1D, fs::LAY_INTER>(h, (FS_T *)c, (FS_T *)cnew, alpha, 1, 0, st, M, 0);
-    if (rc != PB_EUNSUPPORTED) return rc;
-    rc = fc_launch_t<FS_T, 2, true, fs::MODE_CH1D, fs::LAY_INTER>(h, (FS_T *)c, (FS_T *)cnew, alpha, 1, 0, st, M, 0);
     if (rc != PB_EUNSUPPORTED) return rc;
     return fs_launch_t<FS_T, 2, true, fs::MODE_CH1D, fs::LAY_INTER>(h, (FS_T *)c, (FS_T *)cnew, alpha, 1, 0, st, M, 0);
 }
