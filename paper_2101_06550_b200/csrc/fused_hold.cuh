@@ -522,6 +522,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fh_kernel(const __grid_constant__
 #define FHQ(i) do { long long _n = clock64(); pacc[i] += _n - _t; _t = _n; } while (0)
 #else
             long long *pt = nullptr;
+            (void)pt;
 #define FHQ(i) do {} while (0)
 #endif
             for (int t = 0; t < T_; ++t) {

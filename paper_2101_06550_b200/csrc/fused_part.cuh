@@ -300,7 +300,10 @@ static int tp_launch_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
     {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)G);
-        cfg.blockDim = dim3(32 * std::min(tp::SEGMAX, (nq + tp::SL - 1) / tp::SL));
+#ifndef TP_SCAN_WARPS
+#define TP_SCAN_WARPS tp::SEGMAX
+#endif
+        cfg.blockDim = dim3(32 * std::min(TP_SCAN_WARPS, (nq + tp::SL - 1) / tp::SL));
         cfg.dynamicSmemBytes = sms;
         cfg.stream = st;
         cfg.attrs = pdl;
