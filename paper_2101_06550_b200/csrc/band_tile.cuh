@@ -25,11 +25,9 @@ struct FusedScratch {
     void *buf = nullptr;
     size_t bytes = 0;
     int64_t nq = 0, nsys = 0;
-    // two-pass solve (twopass.cuh): records + arrival counters, grow-only; the
-    // counters are zeroed once at allocation and left at zero by every solve
+    // two-pass solve (twopass.cuh): chunk records, cyclic rows, x_l; grow-only
     void *tbuf = nullptr;
     size_t tbytes = 0;
-    int64_t tcnt = 0;   // counters at the head of tbuf (all zero between solves)
     // the last tensor map encoded for this stream, per layout (rhs pointer + shape key)
     uint64_t key[2][6] = {{0, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 0}};
     alignas(64) unsigned char tmap[2][128];

@@ -244,11 +244,11 @@ static int tp_launch_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
     CUtensorMap tmap;
     std::lock_guard<std::mutex> lk(h->fplan.mu);
     FusedScratch &S = h->fplan.scratch[st];
-    // [cnt: tcnt counters, zeroed at allocation][car][spec][xl]
-    const size_t off_car = ((size_t)std::max<int64_t>(G, S.tcnt) * 4 + 255) / 256 * 256;
+    // [car][spec][xl]
+    const size_t off_car = 0;
     const size_t off_spec = off_car + es * (size_t)ntiles * 4 * fs::TW, off_xl = off_spec + es * (size_t)G * 4 * fs::TW;
     const size_t need = off_xl + es * (size_t)G * 2 * fs::TW;
-    if (need > S.tbytes || G > S.tcnt) {
+    if (need > S.tbytes) {
         if (S.tbuf) {
             PB_CUDA_TRY(cudaStreamSynchronize(st));   // queued solves may still use the old scratch
             cudaFree(S.tbuf);
@@ -256,9 +256,7 @@ static int tp_launch_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
             S.tbytes = 0;
         }
         PB_CUDA_TRY(cudaMalloc(&S.tbuf, need));
-        PB_CUDA_TRY(cudaMemsetAsync(S.tbuf, 0, off_car, st));
         S.tbytes = need;
-        S.tcnt = (int64_t)(off_car / 4);
     }
     {
         bool flat = false;
@@ -273,7 +271,6 @@ static int tp_launch_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
     A.rsp = (const T *)h->fplan.rsp;
     A.scal = h->scal;
     A.x = x;
-    A.cnt = (unsigned *)base;
     A.car = (T *)(base + off_car);
     A.spec = (T *)(base + off_spec);
     A.xl = (T *)(base + off_xl);

@@ -68,7 +68,6 @@ struct Args {
     T *car;             // [G][nq][4][TW] chunk records: (yF0, yF1, zB0, zB1) -> (yin0, yin1, zin0, zin1)
     T *spec;            // [G][4][TW] zero-inflow g on the cyclic rows
     T *xl;              // [G][2][TW]
-    unsigned *cnt;      // [G] P1 tiles done (reset to 0 by the group's scan)
     int64_t n, M;       // rows, systems per batch
     int64_t bstride;    // elements between batches
     int64_t pitch;      // elements between rows
@@ -103,21 +102,11 @@ __device__ __forceinline__ TC tile_coords(const Args<T> &A, int64_t t)
     return c;
 }
 
-// a warp's group arrival: its lanes' record stores are ordered before lane
-// 0's release increment by the preceding __syncwarp (the scan warp acquires)
-__device__ __forceinline__ void arrive_release(unsigned *c)
-{
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(c) : "memory");
-}
-
 // P2 sweeps of a full tile column in registers (coefficient rows cp in the
 // band_core layout F0 F1 F2 - B1 B2 Z1 Z2), split so the slot refill can be
 // issued between them: once the forward sweep has run, every value read from
 // the slot has been consumed.  Each recurrence takes its newest carry last.
 constexpr int PD2 = 4;
-#ifndef TP_STORE_TMA
-#define TP_STORE_TMA 1   // P2 writes x by TMA stores from the slot (0: STG from registers)
-#endif
 template <typename T, int K>
 __device__ __forceinline__ void p2_fwd(T (&v)[Q], const T *cp, T y0, T y1)
 {
@@ -614,7 +603,6 @@ __global__ void __launch_bounds__(32 * NC, 1) tp_p2_kernel(const __grid_constant
             for (int e = lane; e < NV; e += 32) dst[e] = src[e];
         }
         __syncwarp();   // cp complete
-#if TP_STORE_TMA
         // x goes back through the slot: the tile column into the slot, one TMA
         // store of the box, and the slot's refill once the store has read it
         if (kmax == Q) {
@@ -648,46 +636,9 @@ __global__ void __launch_bounds__(32 * NC, 1) tp_p2_kernel(const __grid_constant
             }
         }
         __syncwarp();
-#else
-        if (kmax == Q) {
-            TPQ(9);
-            p2_fwd<T, K>(v, cp, yi0, yi1);
-            __syncwarp();   // the slot's values are consumed: refill it
-            if (lane == 0 && i + R * NWT < A.ntiles) issue(i + R * NWT, r, true);
-            TPQ(10);
-            p2_bwd<T, K, PER>(v, cp, zi0, zi1, xl0, xl1);
-            TPQ(11);
-        } else {
-            fs::tile_solve<T, K, PER, false>(v, cp, kmax, yi0, yi1, zi0, zi1, xl0, xl1);
-            __syncwarp();
-            if (lane == 0 && i + R * NWT < A.ntiles) issue(i + R * NWT, r, true);
-        }
-        if (PER && K == 2 && r0 + Q > A.n - 2) {
-            const int k2 = (int)(A.n - 2 - r0);
-#pragma unroll
-            for (int kk = 0; kk < Q; ++kk) {
-                if (kk == k2) v[kk] = xl0;
-                if (kk == k2 + 1) v[kk] = xl1;
-            }
-        }
-        __syncwarp();   // cp is rewritten by the next tile
-        const int64_t s = (int64_t)gl * TW + lane;
-        if (s < A.M) {
-            int64_t P = A.pitch;
-            asm volatile("" : "+l"(P));
-            T *x = A.x + (int64_t)b * A.bstride + r0 * P + s;
-#pragma unroll
-            for (int kk = 0; kk < Q; ++kk) {
-                if (kmax == Q || kk < kmax) __stcs(x, v[kk]);
-                x += P;
-            }
-        }
-#endif
         TPQ(12);
     }
-#if TP_STORE_TMA
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-#endif
     TPQ_DONE;
 }
 
