@@ -504,6 +504,79 @@ def bench_coarsen(args, dev):
             "mean_F_first_last": [f0, f1]}
 
 
+def bench_regimes(args, dev):
+    """SURVEY §8(f)3 solver regimes, each a step of stencil RHS + batched solve
+    composed from the library calls (explicit half by stencil_apply, implicit
+    half by the factor-once solve), 2^16 interleaved systems x N = 1024, fp64:
+      cn_tri    CN diffusion, tridiagonal Thomas / Sherman–Morrison
+      cn_penta  CN hyperdiffusion, uniform pentadiagonal
+      rewrite   per-system pentadiagonal LHS re-factored every step, then solved
+                (cuPentBatchRewrite, P:1844-1846)
+    Steps/s and unknowns/s over 50 steps (after 3 warm-up steps)."""
+    import torch
+    import paper_2101_06550_b200 as pb
+
+    n, m, steps = 1024, 1 << 16, 50
+    out = {}
+    x = torch.from_numpy(synth.rhs_uniform(n, m, seed=12)).to(dev).view(n, m)   # [row][system]
+    f = torch.empty_like(x)
+    dx = 1.0 / n
+
+    def timed(step):
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize(dev)
+        e0, e1 = _ev(torch), _ev(torch)
+        e0.record()
+        for _ in range(steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / steps
+
+    st = 1e-4 / (2 * dx * dx)
+    ht = pb.tri_factor_uniform(-st, 1 + 2 * st, -st, batch=m, n=n, periodic=True)
+    wt = np.array([st, 1 - 2 * st, st])
+
+    buf = [x, f]   # the levels swap every step
+
+    def tri_step():
+        pb.stencil_apply(buf[0], buf[1], wt, left=0, right=0, top=1, bottom=1, periodic=True)
+        ht.solve(buf[1])
+        buf.reverse()
+    ms = timed(tri_step)
+    out["cn_tri"] = {"ms_per_step": round(ms, 4), "Munknowns_s": round(n * m / (ms * 1e-3) / 1e6, 1)}
+    ht.close()
+    sp = 1e-8 / (2 * dx ** 4)
+    hp = pb.pent_factor_uniform(sp, -4 * sp, 1 + 6 * sp, -4 * sp, sp, batch=m, n=n, periodic=True)
+    wp = np.array([-sp, 4 * sp, 1 - 6 * sp, 4 * sp, -sp])
+
+    def pent_step():
+        pb.stencil_apply(buf[0], buf[1], wp, left=0, right=0, top=2, bottom=2, periodic=True)
+        hp.solve(buf[1])
+        buf.reverse()
+    ms = timed(pent_step)
+    out["cn_penta"] = {"ms_per_step": round(ms, 4), "Munknowns_s": round(n * m / (ms * 1e-3) / 1e6, 1)}
+    hp.close()
+    mr = 1 << 14
+    a, b, c, d, e = (torch.from_numpy(v).to(dev) for v in synth.dd_penta(n, mr, seed=13))
+    hr = pb.pent_factor(a, b, c, d, e, batch=mr, n=n, lhs_count=mr, periodic=False)
+    xr = torch.from_numpy(synth.rhs_uniform(n, mr, seed=14)).to(dev)
+
+    def rewrite_step():
+        hr.refactor(a, b, c, d, e)
+        hr.solve(xr)
+    ms = timed(rewrite_step)
+    out["rewrite"] = {"ms_per_step": round(ms, 4), "Munknowns_s": round(n * mr / (ms * 1e-3) / 1e6, 1),
+                      "batch": mr}
+    hr.close()
+    del x, f, buf, xr, a, b, c, d, e
+    torch.cuda.empty_cache()
+    out["config"] = {"workload": "SURVEY 8(f)3: 2^16 systems x N=1024 (rewrite: 2^14), fp64, 50 steps each",
+                     "step": "stencil_apply + solve (CN); refactor + solve (rewrite)"}
+    return out
+
+
 def bench_cfg3(args, dev):
     """configs[2]: one 1024^2 simulation (L = 8 pi), 1000 steps = 100 replays of a
     10-step CUDA graph (launch-latency bound: 4 launches per step)."""
@@ -645,6 +718,7 @@ def run_ours(args):
     cfg3 = _leg(bench_cfg3, args, dev) if (not args.no_adi and rank == 0) else None
     ch1d = _leg(bench_ch1d, args, dev) if (not args.no_ch1d and rank == 0) else None
     coarsen = _leg(bench_coarsen, args, dev) if (not args.no_adi and rank == 0) else None
+    regimes = _leg(bench_regimes, args, dev) if (not args.no_sweep and rank == 0) else None
     dist_adi = _leg(bench_dist_adi, args, rank, world, dev) if not args.no_dist else None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -670,7 +744,7 @@ def run_ours(args):
                        "parallelism": f"independent batches x{world}"},
             "roofline": r["roofline"], "cpu_baseline": cpu, "e2e": r["e2e"], "gpu_launches": r["launches"],
             "clocks": r["clocks"], "residual": r["residual"], "sweep": sweep, "ch_adi": adi, "cfg3": cfg3,
-            "ch1d": ch1d, "coarsen": coarsen, "dist_adi": dist_adi,
+            "ch1d": ch1d, "coarsen": coarsen, "regimes": regimes, "dist_adi": dist_adi,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
