@@ -476,12 +476,16 @@ static int fs_launch_t(const Band *h, T *x, T *xout, double alpha, int64_t count
 }
 
 
-// the two-pass kernels unless the held-tile kernel keeps all its warps busy
-// (5 <= N/64 <= 8) or the batch is too small to stream (N/64 <= 4, fewer
-// than 32 K systems: one launch instead of three)
-static inline bool use_twopass(int nq, int64_t systems)
+// the two-pass kernels unless the batch is too small to stream (fewer than
+// 32 K systems of N/64 <= 8: one launch instead of three) or, interleaved,
+// the held-tile kernel keeps all its warps busy (5 <= N/64 <= 8: 0.58 vs
+// 0.70 ms at 512 x 262 144; contiguous 512 x 262 144, the ADI x-sweep, is the
+// other way round: cfg4 step 3.16 -> 3.08 ms)
+static inline bool use_twopass(int nq, int64_t systems, int lay = fs::LAY_INTER)
 {
-    return nq > fh::NW || (nq >= 2 && nq <= fh::NW / 2 && systems >= 32768);
+    if (nq > fh::NW) return true;
+    if (nq < 2 || systems < 32768) return false;
+    return lay == fs::LAY_CONTIG || nq <= fh::NW / 2;
 }
 
 template <typename T, int LAY>
@@ -496,7 +500,7 @@ static int fs_launch_dl(const Band *h, void *x, int64_t count, int64_t bstride, 
     // exchange of the held-tile kernel at N = M = 8192)
     // (and for N/64 <= 4 in the bandwidth regime: the held-tile CTA then runs
     // at most half its warps; 2^20 x 256 fp64: 1.52 vs 1.80 ms)
-    if (use_twopass(h->fplan.nq, (M > 0 ? M : h->batch) * count)) {
+    if (use_twopass(h->fplan.nq, (M > 0 ? M : h->batch) * count, LAY)) {
         if (h->K == 2)
             rc = h->periodic ? tp_launch_t<T, 2, true, LAY>(h, X, count, bstride, st, M, pitch)
                              : tp_launch_t<T, 2, false, LAY>(h, X, count, bstride, st, M, pitch);
@@ -531,7 +535,7 @@ int FS_NAME(const Band *h, void *x, int64_t count, int64_t bstride, cudaStream_t
 int FS_INFO_NAME(const Band *h, int64_t M, int64_t count, int *info)
 {
     int rc;
-    if (use_twopass(h->fplan.nq, M * count) && h->fplan.nq <= tp::SL * tp::NSEG &&
+    if (use_twopass(h->fplan.nq, M * count, FS_LAY) && h->fplan.nq <= tp::SL * tp::NSEG &&
         (int64_t)h->fplan.nq * ((M + fs::TW - 1) / fs::TW) * count < ((int64_t)1 << 31)) {
         // the two-pass kernels: no clusters; info[2] = CTAs of P1
         const int64_t nt = (int64_t)h->fplan.nq * ((M + fs::TW - 1) / fs::TW) * count;

@@ -255,10 +255,11 @@ def test_cluster_and_global_paths(n, sigma, dtype):
     assert relerr(x.double().cpu().numpy(), ref) <= tol
 
 
-@pytest.mark.parametrize("n,m,layout", [(256, 65536, "interleaved"), (200, 40000, "contiguous"), (128, 32768, "interleaved")])
+@pytest.mark.parametrize("n,m,layout", [(256, 65536, "interleaved"), (200, 40000, "contiguous"), (128, 32768, "interleaved"),
+                                        (512, 40000, "contiguous")])
 def test_twopass_short_systems_large_batch(n, m, layout):
-    """N/64 <= 4 with >= 32 K systems takes the two-pass kernels (the held-tile
-    CTA would idle half its warps); sampled systems against the oracle."""
+    """N/64 <= 4 (interleaved) or <= 8 (contiguous) with >= 32 K systems takes
+    the two-pass kernels; sampled systems against the oracle."""
     s = synth.SIGMA_STATS
     diags = synth.const_penta(n, s, -4 * s, 1 + 6 * s, -4 * s, s)
     h = pb.pent_factor(*[torch.from_numpy(v).cuda() for v in diags], batch=m, n=n, periodic=True)
