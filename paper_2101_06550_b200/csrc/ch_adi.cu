@@ -38,7 +38,7 @@ namespace pb {
 // thread = column slides down the rows with the 13-point / 5-point windows in
 // registers (one new Cbar row and one new C^3 - C row per output).  R is fp64.
 #ifndef RHS_RT_J
-#define RHS_RT_J 16
+#define RHS_RT_J 8
 #endif
 #ifndef RHS_RT_I
 #define RHS_RT_I 128
@@ -96,7 +96,10 @@ __global__ void __launch_bounds__(RT_I) adi_rhs_kernel(const TS *__restrict__ cn
     const TS *Cm = cm + (int64_t)blockIdx.z * plane_in;
     double *Ro = R + (int64_t)blockIdx.z * rows * n;
     // ---- stage (all loads of a batch first, then the stores)
-    constexpr int NE = RS_J * RS_I, PER = (NE + RT_I - 1) / RT_I, BATCH = 12;
+#ifndef RHS_BATCH
+#define RHS_BATCH 8
+#endif
+    constexpr int NE = RS_J * RS_I, PER = (NE + RT_I - 1) / RT_I, BATCH = RHS_BATCH;
 #pragma unroll
     for (int u0 = 0; u0 < PER; u0 += BATCH) {
         TS a[BATCH], b[BATCH];

@@ -1,7 +1,7 @@
 mkdir -p gpurun_out
 python -c "import torch; torch.zeros(1).cuda()"
 cp paper_2101_06550_b200/libpentab.so /tmp/orig.so
-for v in orig I64 I256 I64J32; do
+for v in orig B21 B42 B8J8; do
  if [ $v != orig ]; then cp tools/variants/v_$v.so paper_2101_06550_b200/libpentab.so; fi
  echo "== $v"
  timeout 300 python tools/adi_sweep.py 512 2>&1 | tail -1
