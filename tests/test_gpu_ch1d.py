@@ -100,3 +100,24 @@ def test_table_6_1_on_gpu():
         if n * 2 in E and n <= 1024:
             assert abs(math.log2(E[n] / E[2 * n]) - order) <= 5e-5
     print(f"order at 2048 (E_2048 / E_4096): {math.log2(E[2048] / E[4096]):.4f} (paper 2.0005, reading r23)")
+
+
+@pytest.mark.parametrize("n,m", [(256, 32768), (200, 32768), (1000, 64)])
+def test_ch1d_large_and_long_batches(n, m):
+    """The bench's batch shape at reduced size (32 K systems, N = 256 and a
+    ragged 200) and a longer system (N = 1000: a cluster of held-tile CTAs);
+    sampled systems of a 3-step run against the oracle (dx = 2 pi / 256 as in
+    test_ch1d_parity_fp64, where fp64 parity <= 1e-12 is attainable)."""
+    L = n * 2 * math.pi / 256
+    dt = synth.ch_dt(n, L)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n + m)
+    c0 = (torch.rand((n, m), dtype=torch.float64, device="cuda", generator=g) * 0.2 - 0.1)
+    st = pb.CH1DState(c0)
+    pb.ch1d_step(st, dt, gamma=0.01, L=L, nsteps=3)
+    torch.cuda.synchronize()
+    got = st.c.cpu().numpy()
+    C0 = c0.cpu().numpy()
+    for s in sorted({0, 1, 31, 32, m // 2, m - 1}):
+        ref = oracle.ch1d_steps(np.ascontiguousarray(C0[:, s]), 3, n=n, m=1, dt=dt, gamma=0.01, L=L)
+        assert relerr(got[:, s], ref) <= 1e-12, s
