@@ -219,15 +219,18 @@ static int tp_launch_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
     auto k1 = tp::tp_p1_kernel<T, K, PER, NC, R, LAY>;
     auto k2 = tp::tp_p2_kernel<T, K, PER, NC2, R2, LAY>;
     auto ks = tp::tp_scan_kernel<T, K, PER>;
+    auto ks8 = tp::tp_scan_kernel<T, K, PER, 8>;
     const size_t sm1 = sizeof(tp::P1Smem<T, NC, R>) + 1024;
     const size_t sm2 = sizeof(tp::P2Smem<T, NC2, R2>) + 1024;
-    const size_t sms = (sizeof(tp::ScanSmem<T>) + 15) / 16 * 16 + sizeof(T) * 12 * (size_t)h->fplan.nq;
+    const int slt = h->fplan.nq <= 8 ? 8 : tp::SL, nsg = (h->fplan.nq + slt - 1) / slt;
+    const size_t sms = sizeof(T) * tp::scan_smem_elems<T>(nsg, h->fplan.nq);
     if (h->fplan.nq > tp::SL * tp::NSEG) return PB_EUNSUPPORTED;   // longer systems: the global kernel serves
     static std::once_flag once;
     static cudaError_t attr = cudaSuccess;
     std::call_once(once, [&] {
         attr = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
         if (attr == cudaSuccess) attr = cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        if (attr == cudaSuccess) attr = cudaFuncSetAttribute(ks8, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         if (attr == cudaSuccess) attr = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
         cudaGetLastError();
     });
@@ -305,7 +308,8 @@ static int tp_launch_t(const Band *h, T *x, int64_t count, int64_t bstride, cuda
         cfg.stream = st;
         cfg.attrs = pdl;
         cfg.numAttrs = 1;
-        PB_CUDA_TRY(cudaLaunchKernelEx(&cfg, ks, A));
+        if (nq <= 8) PB_CUDA_TRY(cudaLaunchKernelEx(&cfg, ks8, A));
+        else PB_CUDA_TRY(cudaLaunchKernelEx(&cfg, ks, A));
         PB_LAUNCH_CHECK();
     }
     cudaLaunchConfig_t cfg = {};

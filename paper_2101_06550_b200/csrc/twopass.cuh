@@ -354,35 +354,56 @@ __global__ void __launch_bounds__(32 * NC, 1) tp_p1_kernel(const __grid_constant
 constexpr int SL = 16;      // chunks per segment
 constexpr int SEGMAX = 8;   // warps per CTA (the full register budget each)
 constexpr int NSEG = 32;    // segments per group: nq <= 512 (a warp folds segments w, w + 8, ...)
+// shared memory of one scan CTA, sized by its segment count nsg:
+// a, b, ys [nsg][TW][2] | m [nsg][12] (P, Pb, Kc) | gv [4][TW] | chunk maps ct[nq][12]
 template <typename T>
-struct ScanSmem {
-    T a[NSEG][TW][2], b[NSEG][TW][2], ys[NSEG][TW][2];
-    T m[NSEG][12];          // P, Pb, Kc per segment
-    T gv[4][TW];
-    // followed by the chunk maps ct[nq][12]
+struct ScanView {
+    T (*a)[TW][2];
+    T (*b)[TW][2];
+    T (*ys)[TW][2];
+    T (*m)[12];
+    T (*gv)[TW];
+    T *ctm;
 };
+template <typename T>
+__host__ __device__ inline size_t scan_smem_elems(int nsg, int nq)
+{
+    return ((size_t)nsg * (TW * 2 * 3 + 12) + 4 * TW + 1) / 2 * 2 + (size_t)nq * 12;
+}
 
-template <typename T, int K, bool PER>
-__global__ void __launch_bounds__(32 * SEGMAX, 1) tp_scan_kernel(const Args<T> A)
+// SLT: chunks per segment (SL; 8 for systems of <= 8 chunks, whose records
+// then need half the registers: more resident warps)
+template <typename T, int K, bool PER, int SLT = SL>
+__global__ void __launch_bounds__(32 * SEGMAX, SLT <= 8 ? 2 : 1) tp_scan_kernel(const Args<T> A)
 {
     extern __shared__ __align__(16) unsigned char tp_scan_smem[];
-    ScanSmem<T> &sm = *reinterpret_cast<ScanSmem<T> *>(tp_scan_smem);
-    T *ctm = reinterpret_cast<T *>(tp_scan_smem + (sizeof(ScanSmem<T>) + 15) / 16 * 16);
+    const int nsg0 = (A.nq + SLT - 1) / SLT;
+    ScanView<T> sm;
+    {
+        T *p = reinterpret_cast<T *>(tp_scan_smem);
+        sm.a = reinterpret_cast<T(*)[TW][2]>(p);
+        sm.b = sm.a + nsg0;
+        sm.ys = sm.b + nsg0;
+        sm.m = reinterpret_cast<T(*)[12]>(sm.ys + nsg0);
+        sm.gv = reinterpret_cast<T(*)[TW]>(sm.m + nsg0);
+        sm.ctm = p + (((size_t)nsg0 * (TW * 2 * 3 + 12) + 4 * TW + 1) / 2 * 2);   // 16-byte aligned
+    }
+    T *ctm = sm.ctm;
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     for (int e = threadIdx.x; e < A.nq * 12; e += blockDim.x) ctm[e] = A.ct[e];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
-    const int nsg = (A.nq + SL - 1) / SL;
+    const int nsg = (A.nq + SLT - 1) / SLT;
     const int64_t g = blockIdx.x;
     T *cg0 = A.car + g * A.nq * 4 * TW + lane;
     __syncthreads();
     asm volatile("griddepcontrol.wait;" ::: "memory");
     // ---- pass A: every segment of this warp with zero inflows
     for (int sg = w; sg < nsg; sg += nwarp) {
-        const int c0 = sg * SL, nc = min(SL, A.nq - c0);
+        const int c0 = sg * SLT, nc = min(SLT, A.nq - c0);
         const T *cr = cg0 + (int64_t)c0 * 4 * TW;
-        T r[SL][4];
+        T r[SLT][4];
 #pragma unroll
-        for (int i = 0; i < SL; ++i)
+        for (int i = 0; i < SLT; ++i)
             if (i < nc) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) r[i][e] = __ldcg(cr + (i * 4 + e) * TW);
@@ -390,7 +411,7 @@ __global__ void __launch_bounds__(32 * SEGMAX, 1) tp_scan_kernel(const Args<T> A
         T y0 = T(0), y1 = T(0), b0 = T(0), b1 = T(0);
         T Ph[4] = {T(1), T(0), T(0), T(1)}, Qb[4] = {T(1), T(0), T(0), T(1)}, Kc[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
-        for (int i = 0; i < SL; ++i)
+        for (int i = 0; i < SLT; ++i)
             if (i < nc) {
                 const T *m = ctm + (c0 + i) * 12;
                 T mf[4], mb[4], h[4];
@@ -444,23 +465,23 @@ __global__ void __launch_bounds__(32 * SEGMAX, 1) tp_scan_kernel(const Args<T> A
     const T x0 = sm.b[0][lane][0], x1 = sm.b[0][lane][1];
     // ---- pass B: the walks again from the true (Y, Z) of each of this warp's segments
     for (int sg = w; sg < nsg; sg += nwarp) {
-        const int c0 = sg * SL, nc = min(SL, A.nq - c0);
+        const int c0 = sg * SLT, nc = min(SLT, A.nq - c0);
         T *cr = cg0 + (int64_t)c0 * 4 * TW;
         int qs[4] = {-1, -1, -1, -1};
         if (PER) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) qs[j] = A.srow[j] >= 0 ? (int)(A.srow[j] / Q) - c0 : -1;
         }
-        T r[SL][4], cz[SL][2];
+        T r[SLT][4], cz[SLT][2];
 #pragma unroll
-        for (int i = 0; i < SL; ++i)
+        for (int i = 0; i < SLT; ++i)
             if (i < nc) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) r[i][e] = __ldcg(cr + (i * 4 + e) * TW);
             }
         T y0 = sm.ys[sg][lane][0], y1 = sm.ys[sg][lane][1];
 #pragma unroll
-        for (int i = 0; i < SL; ++i)
+        for (int i = 0; i < SLT; ++i)
             if (i < nc) {
                 const T *m = ctm + (c0 + i) * 12;
                 T mf[4], h[4];
@@ -483,7 +504,7 @@ __global__ void __launch_bounds__(32 * SEGMAX, 1) tp_scan_kernel(const Args<T> A
             }
         T z0 = sm.a[sg][lane][0], z1 = sm.a[sg][lane][1];
 #pragma unroll
-        for (int i = SL - 1; i >= 0; --i)
+        for (int i = SLT - 1; i >= 0; --i)
             if (i < nc) {
                 T mb[4];
                 lds2(ctm + (c0 + i) * 12 + 4, mb[0], mb[1]);
@@ -493,7 +514,7 @@ __global__ void __launch_bounds__(32 * SEGMAX, 1) tp_scan_kernel(const Args<T> A
                 z0 = n0, z1 = n1;
             }
 #pragma unroll
-        for (int i = 0; i < SL; ++i)
+        for (int i = 0; i < SLT; ++i)
             if (i < nc) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) __stcg(cr + (i * 4 + e) * TW, r[i][e]);

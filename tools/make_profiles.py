@@ -29,7 +29,7 @@ if os.path.exists(os.path.join(g, lname)):
 # several units are averaged)
 captures = {f"{tag}_solve.raw.csv": ("pent_solve cfg2 N=M=8192 fp64 (P1, scan, P2)", "pent_solve_f64", 3),
             f"{tag}_solve32.raw.csv": ("pent_solve cfg2 N=M=8192 fp32 (P1, scan, P2)", "pent_solve_f32", 3),
-            f"{tag}_adi.raw.csv": ("one ch_adi_step cfg4 fp64 (rhs, x-sweep, y-sweep, combine)", "adi_step_f64", 4),
+            f"{tag}_adi.raw.csv": ("one ch_adi_step cfg4 fp64 (rhs, x-sweep P1/scan/P2, y-sweep, combine)", "adi_step_f64", 6),
             f"{tag}_ch1d.raw.csv": ("one ch1d_step 2^20 x 256 fp64", "ch1d_f64", 1),
             f"{tag}_stencil.raw.csv": ("stencil_apply 5x5 periodic on 8192^2 fp64", "stencil_f64", 1)}
 rows, traffic = [], {}
