@@ -37,7 +37,7 @@ struct FusedPlan {
     void *rec = nullptr, *ct = nullptr, *rsp = nullptr;
     mutable std::mutex mu;
     mutable std::map<cudaStream_t, FusedScratch> scratch;
-    mutable cudaStream_t pipe[2] = {nullptr, nullptr};   // internal streams of the host-buffer pipeline
+    mutable cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};   // internal streams of the host-buffer pipeline
 };
 
 struct Band {

@@ -635,20 +635,20 @@ static int factor_impl(Band *h, const double *a, const double *b, const double *
 // buffer updated (the host-buffer contract of pentab.h).
 static int pipelined_host_solve(const Band *h, void *host, const pb_layout &L, cudaStream_t st)
 {
-    constexpr int NCHUNK = 8;
+    constexpr int NCHUNK = 16, NS = 3;   // column blocks, streams (H2D of c+2 | solve of c+1 | D2H of c)
     const size_t es = dtype_size(h->dtype);
     const int64_t n = h->n, M = L.n_inner, P = L.row_stride;
     int64_t mc = (M + NCHUNK - 1) / NCHUNK;
     mc = (mc + 31) / 32 * 32;   // whole 32-system tiles, 16-byte pitch
     const int nch = (int)((M + mc - 1) / mc);
     struct Res {
-        cudaStream_t s[2] = {nullptr, nullptr};
-        cudaEvent_t e[3] = {nullptr, nullptr, nullptr};
-        void *buf[2] = {nullptr, nullptr};
+        cudaStream_t s[NS] = {};
+        cudaEvent_t e[NS + 1] = {};
+        void *buf[NS] = {};
         cudaStream_t owner = nullptr;
         ~Res()
         {
-            for (int k = 0; k < 2; ++k)
+            for (int k = 0; k < NS; ++k)
                 if (buf[k]) cudaFreeAsync(buf[k], owner);
             for (auto ev : e)
                 if (ev) cudaEventDestroy(ev);
@@ -656,29 +656,29 @@ static int pipelined_host_solve(const Band *h, void *host, const pb_layout &L, c
     } R;
     R.owner = st;
     {
-        // the handle's two pipeline streams (created once; their scratch is reused)
+        // the handle's pipeline streams (created once; their scratch is reused)
         std::lock_guard<std::mutex> lk(h->fplan.mu);
-        for (int k = 0; k < 2; ++k)
+        for (int k = 0; k < NS; ++k) {
             if (!h->fplan.pipe[k]) PB_CUDA_TRY(cudaStreamCreateWithFlags(&h->fplan.pipe[k], cudaStreamNonBlocking));
-        R.s[0] = h->fplan.pipe[0];
-        R.s[1] = h->fplan.pipe[1];
+            R.s[k] = h->fplan.pipe[k];
+        }
     }
-    for (int k = 0; k < 3; ++k) PB_CUDA_TRY(cudaEventCreateWithFlags(&R.e[k], cudaEventDisableTiming));
+    for (int k = 0; k <= NS; ++k) PB_CUDA_TRY(cudaEventCreateWithFlags(&R.e[k], cudaEventDisableTiming));
     const size_t cbytes = es * (size_t)mc * (size_t)n;
-    for (int k = 0; k < 2; ++k) PB_CUDA_TRY(cudaMallocAsync(&R.buf[k], cbytes, st));
-    PB_CUDA_TRY(cudaEventRecord(R.e[2], st));   // the caller's prior work (and the allocations)
-    for (int k = 0; k < 2; ++k) PB_CUDA_TRY(cudaStreamWaitEvent(R.s[k], R.e[2], 0));
+    for (int k = 0; k < NS; ++k) PB_CUDA_TRY(cudaMallocAsync(&R.buf[k], cbytes, st));
+    PB_CUDA_TRY(cudaEventRecord(R.e[NS], st));   // the caller's prior work (and the allocations)
+    for (int k = 0; k < NS; ++k) PB_CUDA_TRY(cudaStreamWaitEvent(R.s[k], R.e[NS], 0));
     char *hb = (char *)host;
     for (int c = 0; c < nch; ++c) {
-        const int k = c & 1;
+        const int k = c % NS;
         const int64_t s0 = (int64_t)c * mc, m = std::min<int64_t>(mc, M - s0);
-        // block c reuses buffer k after block c-2's D2H (same stream: ordered)
+        // block c reuses buffer k after block c-NS's D2H (same stream: ordered)
         PB_CUDA_TRY(cudaMemcpy2DAsync(R.buf[k], es * m, hb + es * s0, es * P, es * m, n, cudaMemcpyHostToDevice, R.s[k]));
         int rc = launch_fused(h, R.buf[k], PB_INTERLEAVED, 1, 0, R.s[k], m, m);
         if (rc) return rc;
         PB_CUDA_TRY(cudaMemcpy2DAsync(hb + es * s0, es * P, R.buf[k], es * m, es * m, n, cudaMemcpyDeviceToHost, R.s[k]));
     }
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < NS; ++k) {
         PB_CUDA_TRY(cudaEventRecord(R.e[k], R.s[k]));
         PB_CUDA_TRY(cudaStreamWaitEvent(st, R.e[k], 0));
     }
