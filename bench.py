@@ -344,8 +344,8 @@ def bench_penta(args, rank, world, dev):
                              "tp_p2_kernel (3 launches, PDL-chained)", f"pent_solve_{args.dtype}"),
         "e2e": {"value": round(e2e_val, 2), "unit": "Munknowns/s", "steps": e2e_steps,
                 "h2d_bytes_per_step": es * n * m, "d2h_bytes_per_step": es * n * m,
-                "path": "pent_solve(handle, host pinned rhs) -> pitched H2D | fused solve | D2H of 8 column "
-                        "blocks pipelined on 2 streams"},
+                "path": "pent_solve(handle, host pinned rhs) -> pitched H2D | solve | D2H of 16 column "
+                        "blocks pipelined on 3 streams"},
     }
 
 
